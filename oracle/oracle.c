@@ -1,0 +1,139 @@
+/*
+ * ORACLE -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct float64 CPU implementation of the one
+ * computation this repository accelerates.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load it.  The
+ * product path (paper_1405_7470_b200/) never links, imports or executes it,
+ * and this file shares no code, header, table or helper with the CUDA side.
+ *
+ * What it computes (section 2.1, the reduction example):
+ *
+ *     c[i,j] = sum(k, a[i,k]*b[k,j])
+ *
+ * over the loop domain { [i,j,k] : 0<=i<M, 0<=j<N, 0<=k<K }  (P:211-224,
+ * section 2.1: a box over the inames i, j, k with parameters M, N, K).
+ *
+ *  - Inputs are fp32 (section 2.2: type inference, single precision
+ *    in -> single precision out).  Each product of two fp32 values is exact in
+ *    float64 (24+24 <= 53 significant bits), so the only rounding is in the
+ *    float64 sum; k is summed in ascending order (the lexicographic order of
+ *    SPEC.md's reference_run).
+ *  - Layout semantics follow the per-axis stride tags (P:278-280, P:313-315,
+ *    P:594-601): row-major X(r,c) = X[r*ld + c], column-major X(r,c) = X[r + c*ld].
+ *  - K == 0 gives 0 (the identity of `sum`); M == 0 or N == 0 is
+ *    an empty domain and writes nothing.
+ *  - It also returns D[i,j] = sum_k |a[i,k]| |b[k,j]|, the denominator of the
+ *    normalised error of the parity contract (BASELINE.json north_star).
+ *
+ * Outputs are always packed row-major float64 arrays (result row i - row0 at
+ * offset (i - row0)*N).  Parallelism is over i only (OpenMP), so each element's
+ * summation order is fixed and results are bitwise reproducible for any thread
+ * count.  Pins: tests/test_oracle.py (exact rational brute force, closed forms,
+ * worked examples, library cross-check) -- see DESIGN.md "Oracle pins".
+ */
+#include <stdint.h>
+#include <stddef.h>
+#include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_ROW_MAJOR 0
+#define ORACLE_COL_MAJOR 1
+
+/* X(r, c) for a matrix stored with `layout` and leading dimension `ld`. */
+static inline double at(const float *X, int64_t ld, int layout, int64_t r, int64_t c)
+{
+    return (double)(layout == ORACLE_ROW_MAJOR ? X[r * ld + c] : X[r + c * ld]);
+}
+
+static int bad_args(int64_t M, int64_t N, int64_t K, int la, int lb)
+{
+    if (M < 0 || N < 0 || K < 0) return 1;
+    if ((la != ORACLE_ROW_MAJOR && la != ORACLE_COL_MAJOR) ||
+        (lb != ORACLE_ROW_MAJOR && lb != ORACLE_COL_MAJOR)) return 1;
+    return 0;
+}
+
+/* Rows [row0, row1) of C = A*B and of D = |A|*|B|.  Returns 0, or -1 on bad
+ * arguments.  nthreads <= 0 uses the OpenMP default. */
+int lpy_oracle_gemm_rows_f64(int64_t M, int64_t N, int64_t K,
+                             const float *A, int64_t lda, int la,
+                             const float *B, int64_t ldb, int lb,
+                             int64_t row0, int64_t row1,
+                             double *C, double *D, int nthreads)
+{
+    if (bad_args(M, N, K, la, lb) || row0 < 0 || row1 > M || row0 > row1) return -1;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+#endif
+    for (int64_t i = row0; i < row1; ++i) {
+        double *c = C + (i - row0) * N;
+        double *d = D ? D + (i - row0) * N : NULL;
+        for (int64_t j = 0; j < N; ++j) {
+            c[j] = 0.0;                       /* sum identity */
+            if (d) d[j] = 0.0;
+        }
+        for (int64_t k = 0; k < K; ++k) {     /* k ascending */
+            const double a = at(A, lda, la, i, k);
+            for (int64_t j = 0; j < N; ++j) {
+                const double b = at(B, ldb, lb, k, j);
+                c[j] += a * b;                /* a*b exact in float64 */
+                if (d) d[j] += fabs(a) * fabs(b);
+            }
+        }
+    }
+    (void)nthreads;
+    return 0;
+}
+
+/* The full product: rows [0, M). */
+int lpy_oracle_gemm_f64(int64_t M, int64_t N, int64_t K,
+                        const float *A, int64_t lda, int la,
+                        const float *B, int64_t ldb, int lb,
+                        double *C, double *D, int nthreads)
+{
+    return lpy_oracle_gemm_rows_f64(M, N, K, A, lda, la, B, ldb, lb, 0, M, C, D, nthreads);
+}
+
+/* Selected elements (ii[e], jj[e]), e < count: the same k-ascending float64 sum
+ * as above, so each value is bitwise identical to the full product's. */
+int lpy_oracle_gemm_elems_f64(int64_t M, int64_t N, int64_t K,
+                              const float *A, int64_t lda, int la,
+                              const float *B, int64_t ldb, int lb,
+                              int64_t count, const int64_t *ii, const int64_t *jj,
+                              double *C, double *D, int nthreads)
+{
+    if (bad_args(M, N, K, la, lb) || count < 0) return -1;
+    for (int64_t e = 0; e < count; ++e)
+        if (ii[e] < 0 || ii[e] >= M || jj[e] < 0 || jj[e] >= N) return -1;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(static) num_threads(nthreads)
+#endif
+    for (int64_t e = 0; e < count; ++e) {
+        double c = 0.0, d = 0.0;
+        for (int64_t k = 0; k < K; ++k) {
+            const double a = at(A, lda, la, ii[e], k);
+            const double b = at(B, ldb, lb, k, jj[e]);
+            c += a * b;
+            d += fabs(a) * fabs(b);
+        }
+        C[e] = c;
+        if (D) D[e] = d;
+    }
+    (void)nthreads;
+    return 0;
+}
+
+/* Number of OpenMP threads a call with nthreads <= 0 would use. */
+int lpy_oracle_max_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

@@ -1,0 +1,33 @@
+"""Reader for the worked-example fixtures under tests/golden/ (each file cites
+the passage its values come from in its header comments)."""
+import os
+
+import numpy as np
+
+GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def golden_files():
+    return sorted(f for f in os.listdir(GOLDEN_DIR) if f.endswith(".txt"))
+
+
+def read_golden(name):
+    lines = [ln.split("#", 1)[0].strip() for ln in open(os.path.join(GOLDEN_DIR, name))]
+    lines = [ln for ln in lines if ln]
+    assert lines[0] == "M N K"
+    M, N, K = (int(x) for x in lines[1].split())
+    pos = 2
+
+    def block(tag, rows):
+        nonlocal pos
+        assert lines[pos] == tag, (name, lines[pos], tag)
+        pos += 1
+        out = np.array([[float(x) for x in lines[pos + r].split()] for r in range(rows)])
+        pos += rows
+        return out
+
+    A = block("A", M)
+    B = block("B", K)
+    C = block("C", M)
+    assert A.shape == (M, K) and B.shape == (K, N) and C.shape == (M, N)
+    return M, N, K, A.astype(np.float32), B.astype(np.float32), C
