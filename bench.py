@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""Benchmark: fp32 C = A*B (Loo.py's reduction example)
+on B200 through the C-ABI, BASELINE.json's metric
+
+    "fp32 GEMM GFLOP/s at n=4096/8192 on 1/2/4/8 B200; % of FMA/TF32 roofline"
+
+One step = one whole distributed product over the n=8192 square workload
+(BASELINE config 4): at N=1 one lpy_gemm_f32 call; at N>1 each rank owns a
+row panel of A and C and B is broadcast from rank 0 with NCCL inside the step
+(chunked along N to overlap the per-block products).  `value` = 2 n^3 per
+step / max-over-ranks device time (strong scaling: total work fixed).
+
+Prints ONE JSON line on rank 0 (contract in the task statement; fields
+documented in DESIGN.md "Measurement").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 8192] [--path auto|ffma|3xtf32]
+  python bench.py --impl reference ...   # the float64 CPU oracle, timed on host cores
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "fp32 GEMM GFLOP/s at n=4096/8192 on 1/2/4/8 B200; % of FMA/TF32 roofline"
+UNIT = "GFLOP/s"
+L2_BYTES = 126 * 2 ** 20
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback"
+
+
+def roofline_peak(path: str):
+    """(bound, peak TFLOP/s, note) for the dominant kernel of `path`.
+
+    3xtf32: tensor bound; TF32 peak = measured bf16 burst x the guide's nominal
+            tf32/bf16 ratio (1.1 / 2.25), divided by 3 because every fp32
+            product costs three tf32 MMAs (frac = tensor-pipe utilisation).
+    ffma  : plain fp32 FMA ("alu") bound: 148 SM x 128 FP32 lanes x 2 flop x
+            max SM clock."""
+    peaks, src = load_peaks()
+    if path == "3xtf32":
+        tf32 = peaks["bf16_tflops"] * (1.1 / 2.25)
+        return "tensor", tf32 / 3.0, (f"TF32 = {src} bf16 burst {peaks['bf16_tflops']} x 1.1/2.25 = "
+                                       f"{tf32:.1f} TFLOP/s; /3 for 3 tf32 MMAs per fp32 product")
+    mhz = peaks.get("sm_max_mhz", 1965.0)
+    return "alu", 148 * 128 * 2 * mhz * 1e6 / 1e12, f"148 SM x 128 FP32 lanes x 2 x {mhz} MHz ({src} clock)"
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.01):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._thread = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            handle = None
+            try:
+                import torch
+                pci = torch.cuda.get_device_properties(device_index).pci_bus_id
+                handle = pynvml.nvmlDeviceGetHandleByPciBusId(pci)
+            except Exception:
+                handle = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self._h = handle
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(handle, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+        self.period = period_s
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._thread:
+            self._thread.join()
+
+    def summary(self):
+        if self._nv is None:
+            return None
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- CPU oracle
+def oracle_sample(n: int, seconds: float, dist_name: str, nthreads: int = 0):
+    """Time the float64 oracle on a bounded sample of the n x n x n product:
+    the first R rows of C (R sized to ~`seconds`).  Returns (GFLOP/s, sample
+    description, threads)."""
+    import numpy as np
+    import oracle
+    import synth
+    B = synth.matrix(n, n, seed=0, matrix_id=synth.MATRIX_B, dist=dist_name).reshape(-1)
+    threads = nthreads or oracle.max_threads()
+    R = max(1, threads)
+    A = synth.matrix(R, n, seed=0, matrix_id=synth.MATRIX_A, dist=dist_name).reshape(-1)
+    t0 = time.perf_counter()
+    oracle.gemm_rows(R, n, n, A, n, 0, B, n, 0, 0, R, nthreads=threads)
+    dt = time.perf_counter() - t0
+    rows = int(max(R, min(n, R * max(1.0, seconds / max(dt, 1e-6)))))
+    rows = (rows // threads) * threads or threads
+    A = synth.matrix(rows, n, seed=0, matrix_id=synth.MATRIX_A, dist=dist_name).reshape(-1)
+    t0 = time.perf_counter()
+    oracle.gemm_rows(rows, n, n, A, n, 0, B, n, 0, 0, rows, nthreads=threads)
+    dt = time.perf_counter() - t0
+    gflops = 2.0 * rows * n * n / dt / 1e9
+    return gflops, dt, f"first {rows} rows of C for n={n} (all of B), float64 i-k-j loop", threads
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle as it stands, timed on this box's host cores."""
+    if rank != 0:
+        return
+    import oracle
+    n = args.n
+    per_step = max(0.5, args.ref_seconds)
+    # calibrate the sample once, then time each step on that fixed sample
+    gf, dt, sample, threads = oracle_sample(n, per_step, "uniform")
+    times = []
+    import numpy as np
+    import synth
+    rows = int(sample.split()[1])
+    B = synth.matrix(n, n, seed=0, matrix_id=synth.MATRIX_B).reshape(-1)
+    A = synth.matrix(rows, n, seed=0, matrix_id=synth.MATRIX_A).reshape(-1)
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.gemm_rows(rows, n, n, A, n, 0, B, n, 0, 0, rows, nthreads=threads)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = sum(times)
+    value = 2.0 * rows * n * n * len(times) / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: seeded SplitMix64 uniform[-1,1) fp32 inputs",
+        "config": {"workload": f"n={n} square C=A*B, row-major (BASELINE config 4), "
+                               f"bounded sample: {rows} rows of C per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def make_inputs(n, rank, world, chunks, device):
+    """This rank's A panel and (on rank 0) B in column-blocked storage."""
+    import numpy as np
+    import torch
+    import synth
+    from paper_1405_7470_b200.dist import chunk_bounds, panel_bounds
+    r0, r1 = panel_bounds(n, world, rank)
+    A = torch.from_numpy(synth.matrix(r1 - r0, n, seed=0, matrix_id=synth.MATRIX_A, row0=r0)).to(device)
+    bounds = chunk_bounds(n, chunks)
+    blocks = []
+    for c0, c1 in bounds:
+        if rank == 0:
+            blk = synth.matrix(n, c1 - c0, seed=0, matrix_id=synth.MATRIX_B, col0=c0)
+            blocks.append(torch.from_numpy(blk).to(device))
+        else:
+            blocks.append(torch.empty((n, c1 - c0), dtype=torch.float32, device=device))
+    C = torch.empty((r1 - r0, n), dtype=torch.float32, device=device)
+    return A, blocks, C, bounds, (r0, r1)
+
+
+def time_path(args, path, rank, world, device, dist_on):
+    import torch
+    import paper_1405_7470_b200 as lpy
+    from paper_1405_7470_b200.dist import rowpanel_gemm
+    n = args.n
+    chunks = args.chunks if world > 1 else 1
+    A, blocks, C, bounds, (r0, r1) = make_inputs(n, rank, world, chunks, device)
+
+    def gemm_fn(a, b, c):
+        lpy.gemm(a, b, out=c, path=path)
+
+    comm = torch.cuda.Stream() if world > 1 else None
+
+    def step():
+        if world == 1:
+            lpy.gemm(A, blocks[0], out=C, path=path)
+        else:
+            rowpanel_gemm(A, blocks, C, bounds, gemm_fn=gemm_fn, comm_stream=comm)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist_on:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per = []
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0.record()
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            per.append((e0, e1))
+        t1.record()
+        torch.cuda.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    kernel_ms = [a.elapsed_time(b) for a, b in per]
+    if dist_on:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        total_ms = float(t.item())
+    # sampled parity of this run's output against the oracle (rank 0 panel)
+    parity = None
+    if rank == 0 and not args.no_parity:
+        parity = sampled_parity(A, blocks, bounds, C, n, r0)
+    _, chosen = lpy.lpy_select_path(r1 - r0, n, n, lpy.PATHS[path])
+    return {"total_ms": total_ms, "kernel_ms": kernel_ms, "clocks": clk.summary(), "parity": parity,
+            "path": {1: "ffma", 2: "3xtf32"}[chosen], "launches_per_step": len(bounds)}
+
+
+def sampled_parity(A, blocks, bounds, C, n, r0, count=512):
+    import numpy as np
+    import oracle
+    rng = np.random.default_rng(0)
+    rows = A.shape[0]
+    ii = rng.integers(0, rows, count)
+    jj = rng.integers(0, n, count)
+    Ah = A.cpu().numpy().reshape(-1)
+    Bh = np.concatenate([b.cpu().numpy() for b in blocks], axis=1).reshape(-1)
+    Ch = C.cpu().numpy()
+    Cref, D = oracle.gemm_elems(rows, n, n, Ah, n, 0, Bh, n, 0, ii, jj)
+    return oracle.normalized_error(Ch[ii, jj], Cref, D)
+
+
+def time_e2e(args, path, rank, world, device):
+    """Same product end to end through lpy_gemm_f32_host: pinned host A panel
+    and B in, host C panel out, copies inside the timed region."""
+    import torch
+    import paper_1405_7470_b200 as lpy
+    import synth
+    from paper_1405_7470_b200.dist import panel_bounds
+    n = args.n
+    r0, r1 = panel_bounds(n, world, rank)
+    A = torch.from_numpy(synth.matrix(r1 - r0, n, seed=0, matrix_id=0, row0=r0)).pin_memory()
+    B = torch.from_numpy(synth.matrix(n, n, seed=0, matrix_id=1)).pin_memory()
+    C = torch.empty((r1 - r0, n), dtype=torch.float32).pin_memory()
+    s = torch.cuda.current_stream()
+    steps = max(1, min(args.steps, args.e2e_steps))
+
+    def step():
+        lpy.gemm_host(r1 - r0, n, n, A, n, 0, B, n, 0, C, n, 0, path=path, stream=s)
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    h2d = 4 * ((r1 - r0) * n + n * n) * world
+    d2h = 4 * (r1 - r0) * n * world
+    return {"value": 2.0 * n ** 3 / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--path", default="auto", choices=["auto", "ffma", "3xtf32"])
+    ap.add_argument("--also", default="ffma", help="secondary path to report ('' for none)")
+    ap.add_argument("--chunks", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-seconds", type=float, default=4.0)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import paper_1405_7470_b200 as lpy
+    lpy.load_library()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    dist_on = world > 1
+    if dist_on:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+
+    main_path = args.path
+    if main_path == "auto":
+        _, chosen = lpy.lpy_select_path(args.n, args.n, args.n, lpy.PATH_AUTO)
+        main_path = {1: "ffma", 2: "3xtf32"}[chosen]
+    res = time_path(args, main_path, rank, world, device, dist_on)
+    also = None
+    if args.also and args.also != main_path:
+        also = time_path(args, args.also, rank, world, device, dist_on)
+    e2e = time_e2e(args, main_path, rank, world, device)
+
+    if rank == 0:
+        n = args.n
+        flops = 2.0 * n ** 3
+        ms = res["total_ms"] / args.steps
+        value = flops / (ms * 1e-3) / 1e9
+
+        def roof(r, path):
+            bound, peak, note = roofline_peak(path)
+            kms = statistics.mean(r["kernel_ms"]) if world == 1 else None
+            if kms is None:        # multi-GPU: per-rank panel product time is not isolated
+                return {"bound": bound, "achieved": None, "peak": peak, "unit": "TFLOP/s",
+                        "frac": None, "traffic": None, "peak_note": note}
+            achieved = flops / (kms * 1e-3) / 1e12
+            return {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3),
+                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                    "peak_note": note, "kernel_ms_mean": round(kms, 4)}
+
+        cpu = None
+        if not args.no_cpu and world == 1:
+            gf, dt, sample, threads = oracle_sample(n, args.cpu_seconds, "uniform")
+            cpu = {"value": round(gf, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
+                   "sample": sample, "seconds": round(dt, 2)}
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: seeded SplitMix64 uniform[-1,1) fp32 on a 2^-23 grid",
+            "config": {"workload": f"n={n} square fp32 C=A*B, row-major A/B/C (BASELINE config 4)",
+                       "path": res["path"], "M": n, "N": n, "K": n,
+                       "parallelism": f"rowpanel{world}" + (f"+bcast_chunks{args.chunks}" if world > 1 else ""),
+                       "l2": "inputs larger than L2 (A, B, C 268 MB each > 126 MB), no flush"},
+            "roofline": roof(res, res["path"]),
+            "cpu_baseline": cpu,
+            "e2e": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in e2e.items()},
+            "gpu_launches": res["launches_per_step"] * args.steps,
+            "clocks": res["clocks"],
+            "parity_sampled_max_norm_err": res["parity"],
+        }
+        if also is not None:
+            ams = also["total_ms"] / args.steps
+            line["alt_path"] = {"path": also["path"], "value": round(flops / (ams * 1e-3) / 1e9, 1),
+                                "ms_per_step": round(ams, 4), "roofline": roof(also, also["path"]),
+                                "parity_sampled_max_norm_err": also["parity"], "clocks": also["clocks"]}
+        print(json.dumps(line), flush=True)
+    if dist_on:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,144 @@
+/*
+ * lpy.h -- C ABI of the B200-native fp32 GEMM after Loo.py (Kloeckner,
+ * "Loo.py: transformation-based code generation for GPUs and CPUs",
+ * ARRAY'14, arXiv:1405.7470).  Citations "P:n" are lines of the paper text
+ * (/root/reference/PAPER.md); "S:n" lines of SPEC.md.  Implementation:
+ * paper_1405_7470_b200/csrc/.  Python binding with the same names:
+ * paper_1405_7470_b200/__init__.py.
+ *
+ * THE OPERATION.  The paper's reduction example
+ *
+ *     c[i,j] = sum(k, a[i,k]*b[k,j])                  (section 2.1)
+ *
+ * over the loop domain {[i,j,k]: 0<=i<M, 0<=j<N, 0<=k<K} whose parameters
+ * M, N, K are passed by value at call time.  fp32 inputs give
+ * fp32 outputs (type inference).  C is OVERWRITTEN (pure
+ * assignment, no alpha/beta: the instruction is a plain assignment).
+ * The order of the k summation is unspecified (unordered semantics,
+ * P:395-401); results are accurate to
+ *     max_ij |C_ij - Cexact_ij| / sum_k |A_ik||B_kj|  <=  1e-5
+ * on either path, and exact when every input and partial sum is an integer
+ * representable in fp32 and tf32 (readings A1, A2).
+ *
+ * LAYOUT.  Every operand carries a stride tag (P:278-280, P:313-315,
+ * P:594-601, sections 2.1 and 2.4.3):
+ *     LPY_ROW_MAJOR:  X(r,c) = X[r*ld + c],  ld >= max(1, cols)
+ *     LPY_COL_MAJOR:  X(r,c) = X[r + c*ld],  ld >= max(1, rows)
+ * A is M x K, B is K x N, C is M x N (logical shapes).  Leading dimensions
+ * and element counts are in ELEMENTS (floats), not bytes.  Padding between
+ * lines (ld > minor extent, "padding") is never read or written.
+ *
+ * OWNERSHIP.  The caller owns A, B, C.  For the device entry points they are
+ * device memory of the CURRENT CUDA device (e.g. torch tensors); the library
+ * never frees, reallocates or retains them beyond the enqueued work.  Internal
+ * scratch (the aligned repack of an operand whose base is not 16-byte aligned
+ * or whose ld is not a multiple of 4) is stream-ordered (cudaMallocAsync /
+ * cudaFreeAsync on the caller's stream).
+ *
+ * ASYNCHRONY.  Device entry points enqueue on `stream` (a cudaStream_t passed
+ * as void*; NULL = legacy default stream) and return without synchronising,
+ * like the paper's `evt, (out,) = knl(queue, a=x_dev)`.  Faults in
+ * enqueued work surface at the caller's next synchronisation.
+ *
+ * ERRORS.  Every argument is validated BEFORE anything is enqueued; on any
+ * error return C is untouched and nothing was enqueued (except LPY_ERR_CUDA
+ * raised by a failed launch).  Nothing is thrown across the ABI.  Reentrant;
+ * safe to call from several host threads on different streams.
+ *
+ * DEGENERATE SIZES.  M == 0 or N == 0: empty domain, no-op returning LPY_OK
+ * (S:295).  K == 0: C := 0, the identity of `sum`.
+ */
+#ifndef LPY_H
+#define LPY_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LPY_VERSION 1
+
+typedef enum { LPY_ROW_MAJOR = 0, LPY_COL_MAJOR = 1 } lpy_layout;
+
+/* Which kernel computes the product.
+ *  LPY_PATH_FFMA   : fp32 FFMA on the SIMT pipes -- TMA-staged tiles in shared
+ *                    memory ("add_prefetch"), mbarrier producer /
+ *                    consumer ring, per-thread register micro-tile ("ilp" +
+ *                    "unr").  Each product and sum is an fp32 RN op.
+ *  LPY_PATH_3XTF32 : tcgen05 tensor cores, kind::tf32, with each fp32 operand
+ *                    split x = hi + lo (hi = rna_tf32(x), lo = rna_tf32(x-hi))
+ *                    and C += A_lo B_hi + A_hi B_lo + A_hi B_hi accumulated in
+ *                    TMEM and promoted to fp32 registers periodically.
+ *  LPY_PATH_AUTO   : the library picks (lpy_select_path says which). */
+typedef enum { LPY_PATH_AUTO = 0, LPY_PATH_FFMA = 1, LPY_PATH_3XTF32 = 2 } lpy_path;
+
+typedef enum {
+    LPY_OK = 0,
+    LPY_ERR_INVALID_VALUE = 1,      /* M/N/K < 0 or > INT32_MAX, bad enum value          */
+    LPY_ERR_INVALID_LD = 2,         /* ld below the minimum stated under LAYOUT          */
+    LPY_ERR_NULL_POINTER = 3,       /* NULL operand with a nonzero footprint             */
+    LPY_ERR_MISALIGNED = 4,         /* operand pointer not 4-byte aligned                */
+    LPY_ERR_ALIAS = 5,              /* C's footprint overlaps A's or B's ("restrict",    */
+                                    /* P:354)                                            */
+    LPY_ERR_UNSUPPORTED_DEVICE = 6, /* current device is not compute capability 10.0     */
+    LPY_ERR_OUT_OF_MEMORY = 7,      /* scratch allocation failed                         */
+    LPY_ERR_CUDA = 8,               /* CUDA runtime/driver error: lpy_last_cuda_error()  */
+    LPY_ERR_NOT_SUPPORTED = 9       /* requested path cannot run this problem            */
+} lpy_status;
+
+/* Tuning / test knobs for lpy_gemm_f32_ex.  Zero-initialise for defaults. */
+typedef struct lpy_gemm_opts {
+    int32_t num_ctas;        /* persistent grid size; 0 = one CTA (pair) per SM      */
+    int32_t raster_group;    /* output-tile rows per rasterisation group; 0 = auto   */
+    int32_t promote_kblocks; /* 3xTF32: k-blocks per TMEM partial before promotion;  */
+                             /* 0 = auto                                             */
+    int32_t reserved[5];     /* must be 0                                            */
+} lpy_gemm_opts;
+
+/* C := A * B on the device, enqueued on `stream` (see header comment).
+ * Returns LPY_OK or an lpy_status error. */
+lpy_status lpy_gemm_f32(int64_t M, int64_t N, int64_t K,
+                        const float *A, int64_t lda, lpy_layout layout_a,
+                        const float *B, int64_t ldb, lpy_layout layout_b,
+                        float *C, int64_t ldc, lpy_layout layout_c,
+                        void *stream);
+
+/* As lpy_gemm_f32 with an explicit path and optional knobs (opts may be NULL). */
+lpy_status lpy_gemm_f32_ex(int64_t M, int64_t N, int64_t K,
+                           const float *A, int64_t lda, lpy_layout layout_a,
+                           const float *B, int64_t ldb, lpy_layout layout_b,
+                           float *C, int64_t ldc, lpy_layout layout_c,
+                           void *stream, lpy_path path, const lpy_gemm_opts *opts);
+
+/* End-to-end variant on HOST buffers: copies the logical extents of A and B to
+ * device scratch (stream-ordered, repacked to 16-byte-aligned leading
+ * dimensions on the way), runs lpy_gemm_f32_ex, copies the logical extent of C
+ * back (padding of host C untouched) and SYNCHRONISES `stream` before
+ * returning.  Pinned (page-locked) host buffers give full PCIe bandwidth;
+ * pageable ones work but are slower. */
+lpy_status lpy_gemm_f32_host(int64_t M, int64_t N, int64_t K,
+                             const float *A, int64_t lda, lpy_layout layout_a,
+                             const float *B, int64_t ldb, lpy_layout layout_b,
+                             float *C, int64_t ldc, lpy_layout layout_c,
+                             void *stream, lpy_path path);
+
+/* Host-only: the path `requested` resolves to for this problem shape (no CUDA
+ * calls).  Returns LPY_ERR_INVALID_VALUE for bad enum/sizes. */
+lpy_status lpy_select_path(int64_t M, int64_t N, int64_t K, lpy_path requested,
+                           lpy_path *chosen);
+
+/* Static description of an lpy_status value (never NULL). */
+const char *lpy_status_string(lpy_status s);
+
+/* cudaError_t of this thread's most recent LPY_ERR_CUDA (0 if none). */
+int lpy_last_cuda_error(void);
+
+/* LPY_VERSION of the loaded library. */
+int lpy_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LPY_H */

@@ -1,0 +1,199 @@
+"""paper_1405_7470_b200 -- B200-native fp32 GEMM after Loo.py (arXiv:1405.7470).
+
+Thin Python binding over the C-ABI library ``liblpy.so`` (include/lpy.h).
+Argument marshalling only: every step of the product runs in the library's
+sm_100a kernels.  There is no CPU fallback -- if the library is missing or the
+device is not a B200 the calls fail loudly.
+
+Two layers:
+  * ``lpy_gemm_f32``, ``lpy_gemm_f32_ex``, ``lpy_gemm_f32_host``,
+    ``lpy_select_path``, ``lpy_status_string``, ``lpy_last_cuda_error``,
+    ``lpy_version``: same names and arguments as the C functions (pointers as
+    ints, stream as int/None), returning the raw status.
+  * ``gemm(A, B, out=None, path="auto")`` on torch CUDA tensors, inferring
+    M, N, K from shapes and layout/ld from strides (the paper's size inference,
+    P:366-368, and stride dim_tags), raising ``LpyError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+__all__ = [
+    "ROW_MAJOR", "COL_MAJOR", "PATH_AUTO", "PATH_FFMA", "PATH_3XTF32", "PATHS", "LpyError",
+    "GemmOpts", "library_path", "load_library", "lpy_gemm_f32", "lpy_gemm_f32_ex",
+    "lpy_gemm_f32_host", "lpy_select_path", "lpy_status_string", "lpy_last_cuda_error",
+    "lpy_version", "gemm", "operand_layout", "gemm_host",
+]
+
+ROW_MAJOR = 0
+COL_MAJOR = 1
+PATH_AUTO = 0
+PATH_FFMA = 1
+PATH_3XTF32 = 2
+PATHS = {"auto": PATH_AUTO, "ffma": PATH_FFMA, "3xtf32": PATH_3XTF32}
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_lock = threading.Lock()
+_lib = None
+
+
+def library_path() -> str:
+    return os.path.join(_PKG, "liblpy.so")
+
+
+class GemmOpts(ctypes.Structure):
+    _fields_ = [("num_ctas", ctypes.c_int32), ("raster_group", ctypes.c_int32),
+                ("promote_kblocks", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+
+
+class LpyError(RuntimeError):
+    def __init__(self, status: int, where: str = ""):
+        self.status = status
+        msg = lpy_status_string(status)
+        if status == 8:
+            msg += f" (cudaError {lpy_last_cuda_error()})"
+        super().__init__(f"{where}: {msg}" if where else msg)
+
+
+def load_library():
+    """Load liblpy.so (built by __graft_entry__.build()); raise if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = library_path()
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} is not built; run `python -c 'import __graft_entry__ as g; "
+                               f"g.build()'` (no CPU fallback exists)")
+        lib = ctypes.CDLL(path)
+        i64, i32, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+        gemm_args = [i64, i64, i64, vp, i64, i32, vp, i64, i32, vp, i64, i32, vp]
+        lib.lpy_gemm_f32.argtypes = gemm_args
+        lib.lpy_gemm_f32.restype = i32
+        lib.lpy_gemm_f32_ex.argtypes = gemm_args + [i32, ctypes.POINTER(GemmOpts)]
+        lib.lpy_gemm_f32_ex.restype = i32
+        lib.lpy_gemm_f32_host.argtypes = gemm_args + [i32]
+        lib.lpy_gemm_f32_host.restype = i32
+        lib.lpy_select_path.argtypes = [i64, i64, i64, i32, ctypes.POINTER(i32)]
+        lib.lpy_select_path.restype = i32
+        lib.lpy_status_string.argtypes = [i32]
+        lib.lpy_status_string.restype = ctypes.c_char_p
+        lib.lpy_last_cuda_error.argtypes = []
+        lib.lpy_last_cuda_error.restype = i32
+        lib.lpy_version.argtypes = []
+        lib.lpy_version.restype = i32
+        _lib = lib
+        return lib
+
+
+# ----------------------------------------------------------------- C mirror
+def lpy_gemm_f32(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc, layout_c, stream=None) -> int:
+    return load_library().lpy_gemm_f32(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc, layout_c,
+                                       stream)
+
+
+def lpy_gemm_f32_ex(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc, layout_c, stream=None,
+                    path=PATH_AUTO, opts: GemmOpts | None = None) -> int:
+    return load_library().lpy_gemm_f32_ex(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc,
+                                          layout_c, stream, path,
+                                          ctypes.byref(opts) if opts is not None else None)
+
+
+def lpy_gemm_f32_host(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc, layout_c, stream=None,
+                      path=PATH_AUTO) -> int:
+    return load_library().lpy_gemm_f32_host(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc,
+                                            layout_c, stream, path)
+
+
+def lpy_select_path(M, N, K, requested=PATH_AUTO) -> tuple[int, int]:
+    out = ctypes.c_int(0)
+    st = load_library().lpy_select_path(M, N, K, requested, ctypes.byref(out))
+    return st, out.value
+
+
+def lpy_status_string(status: int) -> str:
+    return load_library().lpy_status_string(status).decode()
+
+
+def lpy_last_cuda_error() -> int:
+    return load_library().lpy_last_cuda_error()
+
+
+def lpy_version() -> int:
+    return load_library().lpy_version()
+
+
+# ----------------------------------------------------------------- torch layer
+def operand_layout(x):
+    """(layout, ld) of a 2-D strided tensor, or None if it is neither row- nor
+    column-major (then the caller must make it contiguous)."""
+    rows, cols = x.shape
+    s0, s1 = x.stride()
+    if (s1 == 1 or cols <= 1) and s0 >= max(1, cols):
+        return ROW_MAJOR, s0
+    if (s0 == 1 or rows <= 1) and s1 >= max(1, rows):
+        return COL_MAJOR, s1
+    if rows <= 1 and cols <= 1:
+        return ROW_MAJOR, 1
+    return None
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _path_id(path) -> int:
+    return PATHS[path] if isinstance(path, str) else int(path)
+
+
+def gemm(A, B, out=None, path="auto", stream=None, opts: GemmOpts | None = None):
+    """C = A @ B for fp32 CUDA tensors through lpy_gemm_f32_ex.  `out` may be
+    row- or column-major (any ld); it is overwritten."""
+    import torch
+    if A.dtype != torch.float32 or B.dtype != torch.float32:
+        raise TypeError("lpy.gemm is fp32 in, fp32 out (PAPER.md P:362-365)")
+    if A.dim() != 2 or B.dim() != 2 or A.shape[1] != B.shape[0]:
+        raise ValueError(f"shape mismatch {tuple(A.shape)} @ {tuple(B.shape)}")
+    if not (A.is_cuda and B.is_cuda):
+        raise ValueError("device tensors required (use gemm_host for host buffers)")
+    M, K = A.shape
+    N = B.shape[1]
+    la = operand_layout(A)
+    if la is None:
+        A = A.contiguous()
+        la = operand_layout(A)
+    lb = operand_layout(B)
+    if lb is None:
+        B = B.contiguous()
+        lb = operand_layout(B)
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    if out.shape != (M, N) or out.dtype != torch.float32:
+        raise ValueError("out must be an fp32 M x N tensor")
+    lc = operand_layout(out)
+    if lc is None:
+        raise ValueError("out must be row- or column-major")
+    st = lpy_gemm_f32_ex(M, N, K, A.data_ptr(), la[1], la[0], B.data_ptr(), lb[1], lb[0],
+                         out.data_ptr(), lc[1], lc[0], _stream_handle(stream), _path_id(path), opts)
+    if st != 0:
+        raise LpyError(st, "lpy_gemm_f32_ex")
+    return out
+
+
+def gemm_host(M, N, K, A, lda, la, B, ldb, lb, C, ldc, lc, path="auto", stream=None):
+    """End-to-end product on host buffers (numpy arrays or CPU torch tensors,
+    ideally pinned) through lpy_gemm_f32_host; synchronises before returning."""
+    def ptr(x):
+        if hasattr(x, "data_ptr"):
+            return x.data_ptr()
+        return x.ctypes.data
+    st = lpy_gemm_f32_host(M, N, K, ptr(A), lda, la, ptr(B), ldb, lb, ptr(C), ldc, lc,
+                           _stream_handle(stream) if stream is not None else None, _path_id(path))
+    if st != 0:
+        raise LpyError(st, "lpy_gemm_f32_host")
+    return C

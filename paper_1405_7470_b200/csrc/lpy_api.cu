@@ -1,0 +1,301 @@
+// C-ABI front end (include/lpy.h): validation, layout canonicalisation,
+// degenerate sizes, aligned repack, path selection, launch, and the host-buffer
+// end-to-end entry point.  No torch types anywhere; plain pointers and sizes.
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/lpy.h"
+#include "lpy_internal.h"
+
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+
+lpy_status cuda_fail(cudaError_t e) {
+    g_last_cuda_error = static_cast<int>(e);
+    if (e == cudaErrorMemoryAllocation) return LPY_ERR_OUT_OF_MEMORY;
+    return LPY_ERR_CUDA;
+}
+
+constexpr int64_t kMaxDim = INT32_MAX;
+constexpr int64_t kMaxLd = (int64_t(1) << 40) / 4 - 1;  // TMA: global strides < 2^40 bytes
+
+struct Operand {
+    const float *p;
+    int64_t rows, cols, ld;
+    int layout;
+    int64_t lines() const { return layout == LPY_ROW_MAJOR ? rows : cols; }
+    int64_t inner() const { return layout == LPY_ROW_MAJOR ? cols : rows; }
+    // footprint in elements: (lines-1)*ld + inner, or 0 for an empty matrix
+    int64_t extent() const { return (rows == 0 || cols == 0) ? 0 : (lines() - 1) * ld + inner(); }
+};
+
+bool valid_layout(int l) { return l == LPY_ROW_MAJOR || l == LPY_COL_MAJOR; }
+
+lpy_status validate_operand(const Operand &o) {
+    const int64_t need = o.inner() > 1 ? o.inner() : 1;
+    if (o.ld < need || o.ld > kMaxLd) return LPY_ERR_INVALID_LD;
+    if (o.extent() > 0) {
+        if (o.p == nullptr) return LPY_ERR_NULL_POINTER;
+        if (reinterpret_cast<uintptr_t>(o.p) & 3) return LPY_ERR_MISALIGNED;
+    }
+    return LPY_OK;
+}
+
+bool overlaps(const Operand &a, const Operand &b) {
+    if (a.extent() == 0 || b.extent() == 0) return false;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(a.p), a1 = a0 + uintptr_t(a.extent()) * 4;
+    const uintptr_t b0 = reinterpret_cast<uintptr_t>(b.p), b1 = b0 + uintptr_t(b.extent()) * 4;
+    return a0 < b1 && b0 < a1;
+}
+
+lpy_status validate_all(int64_t M, int64_t N, int64_t K, const Operand &A, const Operand &B,
+                        const Operand &C, int path, const lpy_gemm_opts *opts) {
+    if (M < 0 || N < 0 || K < 0 || M > kMaxDim || N > kMaxDim || K > kMaxDim)
+        return LPY_ERR_INVALID_VALUE;
+    if (!valid_layout(A.layout) || !valid_layout(B.layout) || !valid_layout(C.layout))
+        return LPY_ERR_INVALID_VALUE;
+    if (path != LPY_PATH_AUTO && path != LPY_PATH_FFMA && path != LPY_PATH_3XTF32)
+        return LPY_ERR_INVALID_VALUE;
+    if (opts) {
+        if (opts->num_ctas < 0 || opts->raster_group < 0 || opts->promote_kblocks < 0)
+            return LPY_ERR_INVALID_VALUE;
+        for (int i = 0; i < 5; ++i)
+            if (opts->reserved[i] != 0) return LPY_ERR_INVALID_VALUE;
+    }
+    lpy_status s;
+    if ((s = validate_operand(A)) != LPY_OK) return s;
+    if ((s = validate_operand(B)) != LPY_OK) return s;
+    if ((s = validate_operand(C)) != LPY_OK) return s;
+    if (overlaps(C, A) || overlaps(C, B)) return LPY_ERR_ALIAS;
+    return LPY_OK;
+}
+
+struct DeviceInfo {
+    int major = 0, minor = 0, sms = 0;
+    bool ok = false;
+};
+
+lpy_status device_info(DeviceInfo &out) {
+    static std::mutex mu;
+    static DeviceInfo cache[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (dev < 0 || dev >= 64) return LPY_ERR_UNSUPPORTED_DEVICE;
+    std::lock_guard<std::mutex> g(mu);
+    if (!cache[dev].ok) {
+        DeviceInfo d;
+        if ((e = cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev)) != cudaSuccess ||
+            (e = cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev)) != cudaSuccess ||
+            (e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+            return cuda_fail(e);
+        d.ok = true;
+        cache[dev] = d;
+    }
+    out = cache[dev];
+    // The kernels are built for sm_100a only (tcgen05 / TMA); anything else would
+    // fail at launch with "no kernel image", so refuse up front.
+    if (!(out.major == 10 && out.minor == 0)) return LPY_ERR_UNSUPPORTED_DEVICE;
+    return LPY_OK;
+}
+
+lpy_path resolve_path(int64_t M, int64_t N, int64_t K, lpy_path requested) {
+    if (requested != LPY_PATH_AUTO) return requested;
+    // 3xTF32 on the tensor cores wins once there is enough work to fill the
+    // machine; tiny problems are launch-latency bound either way.
+    const double work = double(M) * double(N) * double(K);
+    return (lpy::tf32_available() && work >= double(1 << 27)) ? LPY_PATH_3XTF32 : LPY_PATH_FFMA;
+}
+
+}  // namespace
+
+namespace lpy {
+
+using PFN_encodeTiled = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                     const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                     const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    });
+    return fn;
+}
+
+cudaError_t make_tmap_2d(CUtensorMap *tm, const float *base, uint64_t inner, uint64_t outer, uint64_t ld,
+                         uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return cudaErrorNotSupported;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {ld * sizeof(float)};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+}  // namespace lpy
+
+extern "C" {
+
+const char *lpy_status_string(lpy_status s) {
+    switch (s) {
+        case LPY_OK: return "LPY_OK";
+        case LPY_ERR_INVALID_VALUE: return "LPY_ERR_INVALID_VALUE: bad size or enum argument";
+        case LPY_ERR_INVALID_LD: return "LPY_ERR_INVALID_LD: leading dimension below the minor extent";
+        case LPY_ERR_NULL_POINTER: return "LPY_ERR_NULL_POINTER: NULL operand with nonzero extent";
+        case LPY_ERR_MISALIGNED: return "LPY_ERR_MISALIGNED: operand not 4-byte aligned";
+        case LPY_ERR_ALIAS: return "LPY_ERR_ALIAS: C overlaps A or B";
+        case LPY_ERR_UNSUPPORTED_DEVICE: return "LPY_ERR_UNSUPPORTED_DEVICE: need compute capability 10.0 (B200)";
+        case LPY_ERR_OUT_OF_MEMORY: return "LPY_ERR_OUT_OF_MEMORY: scratch allocation failed";
+        case LPY_ERR_CUDA: return "LPY_ERR_CUDA: CUDA error (see lpy_last_cuda_error)";
+        case LPY_ERR_NOT_SUPPORTED: return "LPY_ERR_NOT_SUPPORTED: path cannot run this problem";
+    }
+    return "LPY_ERR_UNKNOWN";
+}
+
+int lpy_last_cuda_error(void) { return g_last_cuda_error; }
+
+int lpy_version(void) { return LPY_VERSION; }
+
+lpy_status lpy_select_path(int64_t M, int64_t N, int64_t K, lpy_path requested, lpy_path *chosen) {
+    if (M < 0 || N < 0 || K < 0 || M > kMaxDim || N > kMaxDim || K > kMaxDim || chosen == nullptr)
+        return LPY_ERR_INVALID_VALUE;
+    if (requested != LPY_PATH_AUTO && requested != LPY_PATH_FFMA && requested != LPY_PATH_3XTF32)
+        return LPY_ERR_INVALID_VALUE;
+    *chosen = resolve_path(M, N, K, requested);
+    return LPY_OK;
+}
+
+lpy_status lpy_gemm_f32_ex(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                           lpy_layout layout_a, const float *B, int64_t ldb, lpy_layout layout_b,
+                           float *C, int64_t ldc, lpy_layout layout_c, void *stream, lpy_path path,
+                           const lpy_gemm_opts *opts) {
+    Operand oa{A, M, K, lda, int(layout_a)}, ob{B, K, N, ldb, int(layout_b)}, oc{C, M, N, ldc, int(layout_c)};
+    lpy_status st = validate_all(M, N, K, oa, ob, oc, int(path), opts);
+    if (st != LPY_OK) return st;
+
+    // Column-major C: C^T (N x M, row-major, ld = ldc) = B^T A^T, where the
+    // transpose of a stored matrix is the same memory with the other layout tag.
+    if (layout_c == LPY_COL_MAJOR) {
+        Operand na{B, N, K, ldb, 1 - int(layout_b)};
+        Operand nb{A, K, M, lda, 1 - int(layout_a)};
+        std::swap(M, N);
+        oa = na;
+        ob = nb;
+    }
+    if (M == 0 || N == 0) return LPY_OK;  // empty domain
+
+    DeviceInfo dev;
+    if ((st = device_info(dev)) != LPY_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+
+    if (K == 0) {  // identity of sum: C := 0 (row-major after canonicalisation)
+        e = cudaMemset2DAsync(C, size_t(ldc) * 4, 0, size_t(N) * 4, size_t(M), s);
+        return e == cudaSuccess ? LPY_OK : cuda_fail(e);
+    }
+
+    const lpy_path chosen = resolve_path(M, N, K, path);
+
+    // Aligned repack (reading A7) of any operand TMA cannot describe directly.
+    float *scratch[2] = {nullptr, nullptr};
+    Operand *ops[2] = {&oa, &ob};
+    for (int i = 0; i < 2; ++i) {
+        Operand &o = *ops[i];
+        if ((reinterpret_cast<uintptr_t>(o.p) & 15) == 0 && (o.ld & 3) == 0) continue;
+        const int64_t ld2 = (o.inner() + 3) & ~int64_t(3);
+        e = cudaMallocAsync(reinterpret_cast<void **>(&scratch[i]), size_t(o.lines() * ld2) * 4, s);
+        if (e != cudaSuccess) {
+            for (int j = 0; j < i; ++j)
+                if (scratch[j]) cudaFreeAsync(scratch[j], s);
+            return cuda_fail(e);
+        }
+        e = lpy::launch_repack(o.p, o.ld, scratch[i], ld2, o.lines(), o.inner(), s);
+        if (e != cudaSuccess) {
+            for (int j = 0; j <= i; ++j)
+                if (scratch[j]) cudaFreeAsync(scratch[j], s);
+            return cuda_fail(e);
+        }
+        o.p = scratch[i];
+        o.ld = ld2;
+    }
+
+    lpy::Problem prob{int(M), int(N), int(K), oa.p, oa.ld, oa.layout, ob.p, ob.ld, ob.layout, C, ldc};
+    lpy::Knobs kn{opts ? opts->num_ctas : 0, opts ? opts->raster_group : 0, opts ? opts->promote_kblocks : 0,
+                  dev.sms};
+    if (chosen == LPY_PATH_3XTF32 && !lpy::tf32_supported(prob)) {
+        st = (path == LPY_PATH_3XTF32) ? LPY_ERR_NOT_SUPPORTED : LPY_OK;
+        if (st == LPY_OK) e = lpy::launch_ffma(prob, kn, s);
+    } else {
+        e = chosen == LPY_PATH_3XTF32 ? lpy::launch_3xtf32(prob, kn, s) : lpy::launch_ffma(prob, kn, s);
+    }
+    for (int i = 0; i < 2; ++i)
+        if (scratch[i]) cudaFreeAsync(scratch[i], s);
+    if (st != LPY_OK) return st;
+    return e == cudaSuccess ? LPY_OK : cuda_fail(e);
+}
+
+lpy_status lpy_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, lpy_layout layout_a,
+                        const float *B, int64_t ldb, lpy_layout layout_b, float *C, int64_t ldc,
+                        lpy_layout layout_c, void *stream) {
+    return lpy_gemm_f32_ex(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc, layout_c, stream,
+                           LPY_PATH_AUTO, nullptr);
+}
+
+lpy_status lpy_gemm_f32_host(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                             lpy_layout layout_a, const float *B, int64_t ldb, lpy_layout layout_b,
+                             float *C, int64_t ldc, lpy_layout layout_c, void *stream, lpy_path path) {
+    Operand oa{A, M, K, lda, int(layout_a)}, ob{B, K, N, ldb, int(layout_b)}, oc{C, M, N, ldc, int(layout_c)};
+    lpy_status st = validate_all(M, N, K, oa, ob, oc, int(path), nullptr);
+    if (st != LPY_OK) return st;
+    if (M == 0 || N == 0) return LPY_OK;
+    DeviceInfo dev;
+    if ((st = device_info(dev)) != LPY_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+    // Device copies with 16-byte-aligned leading dimensions: the H2D copy does
+    // the repack for free.
+    Operand *ops[3] = {&oa, &ob, &oc};
+    float *dev_buf[3] = {nullptr, nullptr, nullptr};
+    int64_t dev_ld[3] = {1, 1, 1};
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+        const Operand &o = *ops[i];
+        dev_ld[i] = o.inner() > 0 ? (o.inner() + 3) & ~int64_t(3) : 4;
+        if (o.extent() == 0) continue;
+        e = cudaMallocAsync(reinterpret_cast<void **>(&dev_buf[i]), size_t(o.lines() * dev_ld[i]) * 4, s);
+        if (e == cudaSuccess && i < 2)
+            e = cudaMemcpy2DAsync(dev_buf[i], size_t(dev_ld[i]) * 4, o.p, size_t(o.ld) * 4,
+                                  size_t(o.inner()) * 4, size_t(o.lines()), cudaMemcpyHostToDevice, s);
+    }
+    if (e == cudaSuccess) {
+        st = lpy_gemm_f32_ex(M, N, K, dev_buf[0], dev_ld[0], layout_a, dev_buf[1], dev_ld[1], layout_b,
+                             dev_buf[2], dev_ld[2], layout_c, stream, path, nullptr);
+        if (st == LPY_OK)
+            e = cudaMemcpy2DAsync(C, size_t(ldc) * 4, dev_buf[2], size_t(dev_ld[2]) * 4,
+                                  size_t(oc.inner()) * 4, size_t(oc.lines()), cudaMemcpyDeviceToHost, s);
+    }
+    for (int i = 0; i < 3; ++i)
+        if (dev_buf[i]) cudaFreeAsync(dev_buf[i], s);
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = e2;
+    if (st != LPY_OK) return st;
+    return e == cudaSuccess ? LPY_OK : cuda_fail(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,47 @@
+// Internal interface between the C-ABI front end (lpy_api.cu) and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace lpy {
+
+// A canonical problem: C is row-major (lpy_api.cu maps a column-major C to
+// the transposed problem C^T = B^T A^T first).  Operand layouts: 0 = row-major,
+// 1 = column-major, as in lpy.h.  After the front end's repack step every
+// operand pointer is 16-byte aligned and every ld a multiple of 4 (TMA).
+struct Problem {
+    int M, N, K;
+    const float *A;
+    int64_t lda;
+    int la;
+    const float *B;
+    int64_t ldb;
+    int lb;
+    float *C;
+    int64_t ldc;
+};
+
+struct Knobs {
+    int num_ctas;         // 0 = auto
+    int raster_group;     // 0 = auto
+    int promote_kblocks;  // 0 = auto
+    int num_sms;          // multiprocessor count of the current device
+};
+
+// 2-D tensor map over a strided matrix: `inner` contiguous elements per line,
+// `outer` lines at stride `ld` elements; box = box_inner x box_outer elements.
+// swizzle128 selects CU_TENSOR_MAP_SWIZZLE_128B (else none).
+cudaError_t make_tmap_2d(CUtensorMap *tm, const float *base, uint64_t inner, uint64_t outer,
+                         uint64_t ld, uint32_t box_inner, uint32_t box_outer, bool swizzle128);
+
+cudaError_t launch_ffma(const Problem &p, const Knobs &k, cudaStream_t s);
+cudaError_t launch_3xtf32(const Problem &p, const Knobs &k, cudaStream_t s);
+bool tf32_supported(const Problem &p);
+bool tf32_available();  // the 3xTF32 kernel is compiled in
+
+// dst[line*ld_dst + e] = src[line*ld_src + e] for line < lines, e < inner.
+cudaError_t launch_repack(const float *src, int64_t ld_src, float *dst, int64_t ld_dst,
+                          int64_t lines, int64_t inner, cudaStream_t s);
+
+}  // namespace lpy

@@ -1,0 +1,97 @@
+"""Multi-GPU row-panel product (BASELINE.json north_star).
+
+C's rows are split into contiguous panels, one per rank (one process per GPU);
+rank r owns rows [r*ceil(M/g), min(M, (r+1)*ceil(M/g))) of A and C
+(reading A14).  Row panels are independent given the whole of B,
+C[rows_r, :] = A[rows_r, :] B, so the only exchange is ONE broadcast of B
+(4*K*N bytes) from the root over NCCL / NVLink; C stays sharded.
+
+To overlap the broadcast with the product, B is held in column-blocked
+storage: `chunks` contiguous blocks, block c a row-major K x w_c matrix
+(the same logical B, different storage -- the paper's layout tags).
+Block c is broadcast on a dedicated communication stream while the compute
+stream multiplies the already-arrived blocks: C[:, cols_c] = A_panel B_c is an
+lpy_gemm_f32 call writing a disjoint column block of C (ldc = N).  Chunk
+widths are multiples of 128 (the output tile) so each block is 16-byte aligned.
+
+The GEMM itself is injected (`gemm_fn`) so the orchestration can be tested
+on CPU with the gloo backend (tests/test_dist.py).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+
+def panel_bounds(M: int, world: int, rank: int) -> tuple[int, int]:
+    """Rows [r0, r1) of C owned by `rank` (contiguous panels of ceil(M/world))."""
+    if world < 1 or not 0 <= rank < world or M < 0:
+        raise ValueError("bad panel request")
+    h = math.ceil(M / world) if M else 0
+    r0 = min(M, rank * h)
+    return r0, min(M, r0 + h)
+
+
+def chunk_bounds(N: int, chunks: int, align: int = 128) -> list[tuple[int, int]]:
+    """Column blocks [c0, c1) covering [0, N): `chunks` blocks (fewer if N is
+    small) whose widths are multiples of `align` except possibly the last."""
+    if N <= 0:
+        return []
+    chunks = max(1, min(chunks, math.ceil(N / align)))
+    w = math.ceil(math.ceil(N / chunks) / align) * align
+    out, c0 = [], 0
+    while c0 < N:
+        out.append((c0, min(N, c0 + w)))
+        c0 += w
+    return out
+
+
+@dataclass
+class PanelTiming:
+    bcast_ms: float
+    total_ms: float
+
+
+def rowpanel_gemm(A_panel, B_blocks, C_panel, bounds, group=None, root=0, gemm_fn=None,
+                  comm_stream=None, broadcast=True):
+    """One distributed product step on this rank.
+
+    A_panel : (rows_r, K) tensor, this rank's rows of A.
+    B_blocks: list of (K, w_c) contiguous tensors, the column blocks of B; valid
+              on `root`, receive buffers elsewhere.  Broadcast in order.
+    C_panel : (rows_r, N) row-major tensor; column block c is written by
+              gemm_fn(A_panel, B_blocks[c], C_panel[:, c0:c1]).
+    bounds  : chunk_bounds(N, len(B_blocks)).
+    Returns the list of per-block "arrived" events (CUDA) or None (CPU).
+    """
+    import torch
+    import torch.distributed as dist
+
+    if gemm_fn is None:
+        from . import gemm as gemm_fn_default
+
+        def gemm_fn(a, b, c):
+            gemm_fn_default(a, b, out=c)
+    on_cuda = A_panel.is_cuda
+    events = []
+    if on_cuda:
+        compute = torch.cuda.current_stream()
+        comm = comm_stream or torch.cuda.Stream()
+        comm.wait_stream(compute)
+        for blk in B_blocks:
+            if broadcast:
+                with torch.cuda.stream(comm):
+                    dist.broadcast(blk, src=root, group=group)
+            ev = torch.cuda.Event()
+            ev.record(comm)
+            events.append(ev)
+        for (c0, c1), blk, ev in zip(bounds, B_blocks, events):
+            compute.wait_event(ev)
+            gemm_fn(A_panel, blk, C_panel[:, c0:c1])
+        return events
+    # CPU (gloo) path: same order, no overlap
+    for (c0, c1), blk in zip(bounds, B_blocks):
+        if broadcast:
+            dist.broadcast(blk, src=root, group=group)
+        gemm_fn(A_panel, blk, C_panel[:, c0:c1])
+    return None

@@ -1,0 +1,121 @@
+"""CPU-side checks of the C-ABI boundary (include/lpy.h): the library loads,
+exports every declared symbol, and validates arguments BEFORE any CUDA call
+(so these run without a GPU; nothing here launches work)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1405_7470_b200 as lpy
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "lpy.h")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__
+    __graft_entry__.build_library()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lpy_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    assert declared_functions() == sorted([
+        "lpy_gemm_f32", "lpy_gemm_f32_ex", "lpy_gemm_f32_host", "lpy_select_path",
+        "lpy_status_string", "lpy_last_cuda_error", "lpy_version"])
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(lpy.library_path())
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+        assert hasattr(lpy, name), f"binding lacks {name}"
+
+
+def test_version_and_status_strings():
+    assert lpy.lpy_version() == 1
+    for code in range(10):
+        s = lpy.lpy_status_string(code)
+        assert s.startswith("LPY_")
+    assert lpy.lpy_status_string(0) == "LPY_OK"
+    assert "UNKNOWN" in lpy.lpy_status_string(99)
+    assert lpy.lpy_last_cuda_error() == 0
+
+
+def test_select_path_is_host_only():
+    assert lpy.lpy_select_path(128, 128, 128, lpy.PATH_AUTO) == (0, lpy.PATH_FFMA)
+    assert lpy.lpy_select_path(8192, 8192, 8192, lpy.PATH_FFMA) == (0, lpy.PATH_FFMA)
+    assert lpy.lpy_select_path(8192, 8192, 8192, lpy.PATH_3XTF32) == (0, lpy.PATH_3XTF32)
+    assert lpy.lpy_select_path(-1, 8, 8)[0] == 1
+    assert lpy.lpy_select_path(8, 8, 8, 7)[0] == 1
+
+
+FAKE = 1 << 40      # never dereferenced: validation fails first
+
+
+def call(M=4, N=4, K=4, A=FAKE, lda=4, la=0, B=FAKE + (1 << 20), ldb=4, lb=0,
+         C=FAKE + (2 << 20), ldc=4, lc=0, path=0, opts=None):
+    return lpy.lpy_gemm_f32_ex(M, N, K, A, lda, la, B, ldb, lb, C, ldc, lc, None, path, opts)
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(M=-1), 1), (dict(K=-3), 1), (dict(N=1 << 31), 1),
+    (dict(la=2), 1), (dict(lc=-1), 1), (dict(path=3), 1),
+    (dict(lda=3), 2), (dict(ldb=0), 2), (dict(ldc=3), 2), (dict(la=1, lda=3), 2),
+    (dict(M=5, la=1, lda=4), 2), (dict(lda=1 << 40), 2),
+    (dict(A=0), 3), (dict(B=0), 3), (dict(C=0), 3),
+    (dict(A=FAKE + 2), 4), (dict(C=FAKE + (2 << 20) + 1), 4),
+    (dict(C=FAKE + 8), 5), (dict(C=FAKE + (1 << 20) - 4), 5),
+])
+def test_validation_errors_precede_cuda(kw, code):
+    assert call(**kw) == code
+
+
+def test_bad_opts_rejected():
+    o = lpy.GemmOpts()
+    o.reserved[2] = 1
+    assert call(opts=o) == 1
+    o = lpy.GemmOpts()
+    o.num_ctas = -2
+    assert call(opts=o) == 1
+
+
+def test_empty_domain_is_noop_without_cuda():
+    # M == 0 or N == 0 returns before any CUDA call; NULL is fine then
+    assert call(M=0, A=0, C=0) == 0
+    assert call(N=0, B=0, C=0) == 0
+    # column-major C with an empty extent
+    assert call(M=0, A=0, C=0, lc=1) == 0
+
+
+def test_null_allowed_for_zero_extent_operand():
+    # K == 0: A and B have no footprint, NULL allowed; C must still be valid.
+    # Without a GPU the call then fails in the device query, never before.
+    st = call(K=0, A=0, B=0)
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by the gpu tests")
+    assert st in (6, 8)
+
+
+def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
+    monkeypatch.setattr(lpy, "_lib", None)
+    monkeypatch.setattr(lpy, "library_path", lambda: str(tmp_path / "missing.so"))
+    with pytest.raises(RuntimeError, match="not built"):
+        lpy.load_library()
+
+
+def test_operand_layout_inference():
+    import torch
+    x = torch.empty(5, 7)
+    assert lpy.operand_layout(x) == (lpy.ROW_MAJOR, 7)
+    assert lpy.operand_layout(x.t()) == (lpy.COL_MAJOR, 7)
+    y = torch.empty(5, 12)[:, :7]
+    assert lpy.operand_layout(y) == (lpy.ROW_MAJOR, 12)
+    assert lpy.operand_layout(torch.empty(6, 8)[::2, ::2]) is None

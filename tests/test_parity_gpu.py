@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA paths through the C-ABI against the float64 oracle on
+the same seeded inputs (BASELINE.json configs + edge cases).  Tolerance: the
+north_star bound max|C - Cref| / sum_k|A_ik||B_kj| <= 1e-5; integer-valued
+inputs must come out exactly."""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1405_7470_b200 as lpy
+import synth
+from gpu_util import TOL, check, oracle_ref, run_gemm
+
+pytestmark = pytest.mark.gpu
+
+PATHS = ["ffma", "3xtf32"]
+LAYOUTS = list(itertools.product((0, 1), (0, 1), (0, 1)))
+EDGE = [1, 2, 3, 7, 8, 9, 15, 16, 17, 31, 32, 33, 127, 128, 129, 255, 256, 257]
+
+
+def inputs(M, N, K, seed=0, dist="uniform"):
+    return (synth.matrix(M, K, seed=seed, matrix_id=synth.MATRIX_A, dist=dist),
+            synth.matrix(K, N, seed=seed, matrix_id=synth.MATRIX_B, dist=dist))
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("la,lb,lc", LAYOUTS)
+def test_tiny_and_edge_shapes_all_layouts(path, la, lb, lc):
+    rng = np.random.default_rng(la * 4 + lb * 2 + lc)
+    shapes = [(1, 1, 1), (3, 5, 7), (129, 257, 33), (128, 128, 32)]
+    shapes += [tuple(int(x) for x in rng.choice(EDGE, 3)) for _ in range(8)]
+    for i, (M, N, K) in enumerate(shapes):
+        A, B = inputs(M, N, K, seed=i)
+        for pad in (0, 3, 4):       # packed, unaligned padding (repack), aligned padding
+            C, pad_ok = run_gemm(A, B, la, lb, lc,
+                                 lda=synth.min_ld(M, K, la) + pad, ldb=synth.min_ld(K, N, lb) + pad,
+                                 ldc=synth.min_ld(M, N, lc) + pad, path=path)
+            assert pad_ok, "kernel wrote outside the logical C"
+            check(C, A, B)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_config1_n128_row_major(path):
+    A, B = inputs(128, 128, 128)
+    C, _ = run_gemm(A, B, path=path)
+    check(C, A, B)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("la,lb", list(itertools.product((0, 1), (0, 1))))
+def test_config2_n1024_four_layouts(path, la, lb):
+    A, B = inputs(1024, 1024, 1024, seed=2)
+    C, _ = run_gemm(A, B, la, lb, path=path)
+    check(C, A, B)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("ld_pad", [0, 3])           # packed ld=777 (repack), padded 780 (direct TMA)
+def test_config5_ragged_colmajor_b(path, ld_pad):
+    M, N, K = 1000, 3000, 777
+    A, B = inputs(M, N, K, seed=5)
+    C, pad_ok = run_gemm(A, B, 0, 1, 0, lda=K + ld_pad, ldb=K + ld_pad, ldc=N, path=path)
+    assert pad_ok
+    check(C, A, B)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("dist", ["uniform01", "wide"])
+def test_stress_distributions(path, dist):
+    A, B = inputs(700, 900, 1100, seed=3, dist=dist)
+    C, _ = run_gemm(A, B, 1, 0, 0, path=path)
+    check(C, A, B)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_integer_valued_inputs_exact(path):
+    A, B = inputs(515, 640, 1031, seed=4, dist="int")
+    for la, lb in itertools.product((0, 1), (0, 1)):
+        C, _ = run_gemm(A, B, la, lb, path=path)
+        check(C, A, B, exact=True)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_closed_forms(path):
+    n = 300
+    B = synth.matrix(n, 170, seed=6, matrix_id=1, dist="int")
+    C, _ = run_gemm(synth.identity(n), B, path=path)
+    assert np.array_equal(C, B)
+    P, perm = synth.permutation(n, seed=2)
+    C, _ = run_gemm(P, B, 1, 0, 1, path=path)
+    assert np.array_equal(C, B[perm])
+    # rank-1 outer product, K = 1 (values tf32-exact so both paths are exact)
+    u = synth.matrix(250, 1, seed=7, dist="int")
+    v = synth.matrix(1, 260, seed=7, matrix_id=1, dist="int")
+    C, _ = run_gemm(u, v, path=path)
+    assert np.array_equal(C, u * v)
+    Z = np.zeros((200, 64), np.float32)
+    C, _ = run_gemm(Z, synth.matrix(64, 100, seed=1), path=path)
+    assert not C.any()
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_degenerate_sizes(path):
+    # K == 0: C := 0; M == 0 / N == 0: no-op
+    C, pad_ok = run_gemm(np.zeros((37, 0), np.float32), np.zeros((0, 45), np.float32),
+                         ldc=48, path=path)
+    assert pad_ok and not C.any() and C.shape == (37, 45)
+    C, _ = run_gemm(np.zeros((0, 5), np.float32), np.ones((5, 9), np.float32), path=path)
+    assert C.shape == (0, 9)
+    C, _ = run_gemm(np.ones((4, 5), np.float32), np.ones((5, 0), np.float32), lc=1, path=path)
+    assert C.shape == (4, 0)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_unaligned_base_pointers_repack(path):
+    A, B = inputs(333, 222, 111, seed=8)
+    C, pad_ok = run_gemm(A, B, 0, 1, 0, path=path, base_offset=1)
+    assert pad_ok
+    check(C, A, B)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_determinism_and_grid_invariance(path):
+    A, B = inputs(1000, 1100, 600, seed=9)
+    ref, _ = run_gemm(A, B, path=path)
+    for _ in range(3):
+        C, _ = run_gemm(A, B, path=path)
+        assert np.array_equal(C, ref)
+    for ctas, group in ((74, 0), (37, 3), (1, 1), (500, 0)):
+        o = lpy.GemmOpts()
+        o.num_ctas = ctas
+        o.raster_group = group
+        C, _ = run_gemm(A, B, path=path, opts=o)
+        assert np.array_equal(C, ref), (ctas, group)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_layout_invariance_bitwise(path):
+    A, B = inputs(260, 270, 280, seed=10)
+    ref, _ = run_gemm(A, B, 0, 0, 0, path=path)
+    for la, lb, lc in LAYOUTS:
+        C, _ = run_gemm(A, B, la, lb, lc, path=path)
+        np.testing.assert_array_equal(C, ref)
+
+
+def test_torch_binding_and_host_entry():
+    A, B = inputs(300, 200, 100, seed=11)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    C = lpy.gemm(dA, dB, path="ffma")
+    Ct = torch.empty(200, 300, device="cuda").t()          # column-major out
+    lpy.gemm(dA.t().contiguous().t(), dB, out=Ct, path="ffma")
+    torch.cuda.synchronize()
+    assert torch.equal(C, Ct)
+    check(C.cpu().numpy(), A, B)
+    # end-to-end on host buffers (lpy_gemm_f32_host)
+    abuf, lda = synth.store(A, 0, 103)
+    bbuf, ldb = synth.store(B, 1, 101)
+    cbuf, ldc = synth.store(np.zeros((300, 200), np.float32), 0, 203, pad_value=np.nan)
+    lpy.gemm_host(300, 200, 100, abuf, lda, 0, bbuf, ldb, 1, cbuf, ldc, 0, path="ffma")
+    Ch = synth.load_logical(cbuf, 300, 200, 0, ldc)
+    assert np.array_equal(Ch, C.cpu().numpy())
+    assert np.isnan(cbuf.reshape(-1)[200:203]).all()      # host C padding untouched
+
+
+def test_errors_on_device():
+    A = torch.zeros(4, 4, device="cuda")
+    with pytest.raises(lpy.LpyError):
+        lpy.gemm(A, A, out=A)                               # alias
+    st = lpy.lpy_gemm_f32_ex(4, 4, 4, A.data_ptr(), 4, 0, A.data_ptr(), 4, 0,
+                             A.data_ptr() + 64 * 4, 2, 0, None, 1, None)
+    assert st == 2
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("n,dist", [(4096, "uniform"), (4096, "uniform01"), (8192, "uniform"),
+                                    (8192, "uniform01")])
+def test_full_size_sampled(path, n, dist):
+    """BASELINE configs 3/4 at full size, in the launch configuration bench.py
+    times: every row/column on a tile boundary plus random entries are checked
+    against the oracle element by element."""
+    A = synth.matrix(n, n, seed=0, matrix_id=0, dist=dist)
+    B = synth.matrix(n, n, seed=0, matrix_id=1, dist=dist)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    C = lpy.gemm(dA, dB, path=path).cpu().numpy()
+    rng = np.random.default_rng(n)
+    edges = np.unique(np.concatenate([np.arange(0, n, 128), np.arange(127, n, 128),
+                                      np.arange(0, n, 224) if n % 224 else [], [n - 1]])).astype(int)
+    ii = np.concatenate([np.repeat(edges[::4], 8), rng.integers(0, n, 3000)])
+    jj = np.concatenate([np.tile(edges[:8], len(edges[::4])), rng.integers(0, n, 3000)])
+    Cref, D = oracle.gemm_elems(n, n, n, A.reshape(-1), n, 0, B.reshape(-1), n, 0, ii, jj)
+    err = oracle.normalized_error(C[ii, jj], Cref, D)
+    assert err <= TOL, err
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("path", PATHS)
+def test_full_size_integer_freivalds(path):
+    """n=8192 integer-valued inputs: exact (bit-exact contract) checked with
+    Freivalds' identity C x == A (B x) in int64, 4 random 0/1 vectors."""
+    n = 8192
+    A = synth.matrix(n, n, seed=1, matrix_id=0, dist="int")
+    B = synth.matrix(n, n, seed=1, matrix_id=1, dist="int")
+    C = lpy.gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), path=path).cpu().numpy()
+    assert np.all(C == np.round(C))
+    Ci, Ai, Bi = C.astype(np.int64), A.astype(np.int64), B.astype(np.int64)
+    rng = np.random.default_rng(0)
+    for _ in range(4):
+        x = rng.integers(0, 2, n).astype(np.int64)
+        assert np.array_equal(Ci @ x, Ai @ (Bi @ x))
