@@ -21,10 +21,13 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import faulthandler
 import statistics
+import subprocess
 import sys
-import threading
 import time
+
+faulthandler.enable()
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
@@ -63,65 +66,75 @@ def roofline_peak(path: str):
 
 
 class ClockSampler:
-    """Samples SM clock + throttle reasons with NVML during the timed region."""
+    """Samples SM clock + throttle reasons with `nvidia-smi -lms` during the
+    timed region (the profiling guide's clocks line)."""
 
-    REASONS = {
-        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
-        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
-        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
-    }
+    FIELDS = ("index,pci.bus_id,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device_index: int, period_s: float = 0.01):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
-        self._thread = None
+    def __init__(self, device_index: int, period_ms: int = 50):
+        import shutil
+        import tempfile
+        self.period = period_ms
+        self.proc = None
+        self.bus = None
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            self._nv = pynvml
-            handle = None
-            try:
-                import torch
-                pci = torch.cuda.get_device_properties(device_index).pci_bus_id
-                handle = pynvml.nvmlDeviceGetHandleByPciBusId(pci)
-            except Exception:
-                handle = pynvml.nvmlDeviceGetHandleByIndex(device_index)
-            self._h = handle
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(handle, pynvml.NVML_CLOCK_SM)
+            import torch
+            p = torch.cuda.get_device_properties(device_index)
+            self.bus = f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
         except Exception:
-            self._nv = None
-        self.period = period_s
-
-    def _run(self):
-        nv = self._nv
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-                for name, bit in self.REASONS.items():
-                    if mask & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(self.period)
+            pass
+        self.smi = shutil.which("nvidia-smi")
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
 
     def __enter__(self):
-        if self._nv is not None:
-            self._thread = threading.Thread(target=self._run, daemon=True)
-            self._thread.start()
+        if self.smi:
+            cmd = [self.smi, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                   f"-lms", str(self.period)]
+            self.proc = subprocess.Popen(cmd, stdout=self.out, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._thread:
-            self._thread.join()
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
 
     def summary(self):
-        if self._nv is None:
+        if not self.smi:
             return None
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+        self.out.flush()
+        rows = []
+        with open(self.out.name) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 10:
+                    rows.append(parts)
+        os.unlink(self.out.name)
+        mine = [r for r in rows if self.bus and r[1].upper().endswith(self.bus[-12:])]
+        rows = mine or rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm = []
+        for r in rows:
+            try:
+                sm.append(float(r[2]))
+            except ValueError:
+                pass
+            for name, val in zip(names, r[6:10]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        loaded = [x for x in sm if x > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": float(rows[0][3]) if rows[0][3].replace('.', '').isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
 
 
 # --------------------------------------------------------------------------- CPU oracle

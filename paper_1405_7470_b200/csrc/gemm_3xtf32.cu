@@ -1,8 +1,351 @@
-// 3xTF32 tcgen05 path -- placeholder until the kernel lands.
+// 3xTF32 tensor-core path of C = A*B (the reduction sum(k, a[i,k]*b[k,j]),
+// PAPER.md P:251-254) on the sm_100a 5th-generation tensor cores.
+//
+// Split precision (readings A9/A10).  The tensor core reads an fp32
+// operand as tf32 by TRUNCATING its low 13 mantissa bits (measured:
+// tests/test_numerics_tmem.py).  So each fp32 x is used as
+//     big   = x                      (the hardware sees trunc_tf32(x))
+//     small = rna_tf32(x - trunc_tf32(x))   (computed here, exact residual rounded)
+// and  a*b ~= a_big*b_small + a_small*b_big + a_big*b_big  (small*small dropped;
+// the small terms go first).  Per product the representation error is below
+// 2^-20 |a||b|.  TMEM accumulation rounds toward zero (measured), so the
+// accumulator is PROMOTED: every `promote` k-blocks the MMA warp closes a TMEM
+// partial (double-buffered, 2 x 256 columns) and the epilogue warps add it into
+// fp32 registers with round-to-nearest.
+//
+// Schedule (Loo.py's split_iname / group-local tags / add_prefetch / precompute,
+// P:499-632, realised the Blackwell way):
+//   * persistent CTAs over 128 x 256 output tiles in grouped raster order;
+//   * warp 0 (one lane): TMA producer, A[128 x 16] + B[16 x 256] fp32 per
+//     k-block into a 4-stage ring ("add_prefetch");
+//   * warps 2-3: split transform, raw stage -> small stage in the same swizzled
+//     layout (an elementwise "precompute" into local memory), then
+//     fence.proxy.async so the tensor core sees it;
+//   * warp 1 (one lane): tcgen05.mma kind::tf32 M=128 N=256 K=8, three per
+//     k-slice, accumulating in TMEM; tcgen05.commit frees the stage and
+//     publishes each partial;
+//   * warps 4-11: promotion + epilogue; each owns 32 TMEM lanes (rows) x 128
+//     columns, accumulates partials in registers, and stores the finished row
+//     segment with predicated 16-byte stores (ragged M/N edges; TMA zero-fill
+//     covers ragged K).
+// Operand smem layouts: K-major tiles use the 64B swizzle (16 fp32 per row);
+// MN-major tf32 tiles must use SWIZZLE_128B_BASE32B (TMA "128B_ATOM_32B").
 #include "lpy_internal.h"
+#include "ptx.cuh"
 
 namespace lpy {
-bool tf32_supported(const Problem &) { return false; }
-bool tf32_available() { return false; }
-cudaError_t launch_3xtf32(const Problem &, const Knobs &, cudaStream_t) { return cudaErrorNotSupported; }
+namespace tf32 {
+
+constexpr int BM = 128, BN = 256, BK = 16;
+constexpr int STAGES = 4;
+constexpr int THREADS = 320;            // 10 warps
+constexpr int COMBO_THREADS = 256;      // warps 2-9: transform + promotion + epilogue
+constexpr int COMBO_WARPS = COMBO_THREADS / 32;
+constexpr uint32_t A_BYTES = BM * BK * 4;            // 8 KB
+constexpr uint32_t B_BYTES = BN * BK * 4;            // 16 KB
+constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;    // 24 KB (TMA transaction per stage)
+constexpr uint32_t STAGE_BYTES = 2 * RAW_BYTES;      // raw + small
+constexpr uint32_t TMEM_COLS = 512;                  // 2 partial buffers x 256 columns
+constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * STAGE_BYTES + 256;
+
+struct Params {
+    int M, N, K;
+    float *C;
+    int64_t ldc;
+    int tiles_m, tiles_n, num_tiles, k_blocks, group, promote;
+    int c_vec;
+};
+
+__device__ __forceinline__ void tile_coords(int t, const Params &p, int &tm, int &tn) {
+    const int per_group = p.group * p.tiles_n;
+    const int g = t / per_group;
+    const int first = g * p.group;
+    const int gsize = min(p.group, p.tiles_m - first);
+    const int r = t - g * per_group;
+    tm = first + r % gsize;
+    tn = r / gsize;
+}
+
+// UMMA descriptor of k-slice `sub` (0/1, 8 elements each) of an operand tile.
+// K-major (64B swizzle): rows of 64 B, 8-row groups at 512 B; the slice starts
+// 32 B into the row.  MN-major (128B_BASE32B): 32-wide MN blocks of 16 k-rows
+// x 128 B (2 KB, LBO), 4-row groups at 512 B (SBO); the slice starts 8 rows in.
+template <bool MN>
+__device__ __forceinline__ uint64_t op_desc(uint32_t tile, int sub) {
+    if constexpr (MN) return umma_sdesc(tile + sub * 1024, 2048, 512, 1);
+    else              return umma_sdesc(tile + sub * 32, 16, 512, 4);
+}
+
+// small = rna_tf32(x - trunc_tf32(x)).  The residual is exact in fp32 and finite
+// for finite x, so round-to-nearest-away on its bit pattern is an integer add of
+// half a tf32 ulp followed by truncation (what cvt.rna.tf32.f32 does, minus its
+// NaN/Inf guard).
+__device__ __forceinline__ float tf32_small(float x) {
+    const float big = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);   // what the MMA sees
+    const uint32_t r = __float_as_uint(x - big);
+    return __uint_as_float((r + 0x1000u) & 0xFFFFE000u);
+}
+
+template <bool AMN, bool BMN>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    uint8_t *stages = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stages + STAGES * STAGE_BYTES);
+    uint64_t *full = bars;                  // TMA -> transform
+    uint64_t *ready = bars + STAGES;        // transform -> MMA
+    uint64_t *empty = bars + 2 * STAGES;    // MMA -> producer
+    uint64_t *accf = bars + 3 * STAGES;     // MMA -> epilogue (partial b complete)
+    uint64_t *acce = accf + 2;              // epilogue -> MMA (partial b drained)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&ready[s], COMBO_WARPS);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&accf[b], 1);
+            mbar_init(&acce[b], COMBO_THREADS);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        tmem_alloc(tmem_slot, TMEM_COLS);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int parts_per_tile = (p.k_blocks + p.promote - 1) / p.promote;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            tma_prefetch_desc(&tmA);
+            tma_prefetch_desc(&tmB);
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                int tm, tn;
+                tile_coords(t, p, tm, tn);
+                const int m0 = tm * BM, n0 = tn * BN;
+                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t *sa = stages + s * STAGE_BYTES;
+                    uint8_t *sb = sa + A_BYTES;
+                    mbar_arrive_expect_tx(&full[s], RAW_BYTES);
+                    const int k0 = kb * BK;
+                    if constexpr (AMN) {
+#pragma unroll
+                        for (int j = 0; j < BM / 32; ++j) tma_load_2d(sa + j * 2048, &tmA, &full[s], m0 + 32 * j, k0);
+                    } else {
+                        tma_load_2d(sa, &tmA, &full[s], k0, m0);
+                    }
+                    if constexpr (BMN) {
+#pragma unroll
+                        for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * 2048, &tmB, &full[s], n0 + 32 * j, k0);
+                    } else {
+                        tma_load_2d(sb, &tmB, &full[s], k0, n0);
+                    }
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_tf32(BM, BN, AMN ? 1 : 0, BMN ? 1 : 0);
+            int s = 0;
+            uint32_t ph = 0;
+            uint32_t npart = 0;   // partials issued by this CTA
+            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    const bool first = (kb % p.promote) == 0;
+                    const uint32_t b = npart & 1;
+                    if (first) {
+                        mbar_wait(&acce[b], ((npart >> 1) & 1) ^ 1);   // buffer drained
+                        tc_fence_after();
+                    }
+                    mbar_wait(&ready[s], ph);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(stages + s * STAGE_BYTES);
+                    const uint32_t sb = sa + A_BYTES;
+                    const uint32_t d = tmem + b * 256;
+#pragma unroll
+                    for (int sub = 0; sub < BK / 8; ++sub) {
+                        const uint64_t a_big = op_desc<AMN>(sa, sub), b_big = op_desc<BMN>(sb, sub);
+                        const uint64_t a_small = op_desc<AMN>(sa + RAW_BYTES, sub);
+                        const uint64_t b_small = op_desc<BMN>(sb + RAW_BYTES, sub);
+                        umma_tf32(d, a_big, b_small, idesc, (first && sub == 0) ? 0u : 1u);
+                        umma_tf32(d, a_small, b_big, idesc, 1u);
+                        umma_tf32(d, a_big, b_big, idesc, 1u);
+                    }
+                    umma_commit(&empty[s]);
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                    if ((kb % p.promote) == p.promote - 1 || kb == p.k_blocks - 1) {
+                        umma_commit(&accf[b]);
+                        ++npart;
+                    }
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------ split transform + promotion + epilogue
+        // Warps 2-9 transform every stage (raw -> small) and, whenever a TMEM
+        // partial is complete, fold it into their fp32 register accumulators
+        // (checked without blocking after each stage; the MMA only needs a
+        // buffer back `promote` stages later).  After a tile's last partial
+        // they store its 128 x 256 block of C.
+        const int ctid = threadIdx.x - 64;       // 0..255
+        const int quad = warp & 3;               // TMEM lanes 32*quad .. +31 (hardware rule)
+        const int half = (warp - 2) >> 2;        // columns 128*half .. +127
+        const uint32_t lane_base = uint32_t(quad * 32) << 16;
+        float acc[128];
+#pragma unroll
+        for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+        int t_prom = blockIdx.x, part = 0;       // next partial to promote: (tile, part)
+        uint32_t np = 0;                         // partials promoted so far
+
+        auto promote_ready = [&](bool block) {
+            while (t_prom < p.num_tiles) {
+                const uint32_t b = np & 1, par = (np >> 1) & 1;
+                if (block) {
+                    mbar_wait(&accf[b], par);
+                } else {
+                    uint32_t ok = lane == 0 ? mbar_test(&accf[b], par) : 0u;
+                    if (!__shfl_sync(0xffffffffu, ok, 0)) return;
+                }
+                tc_fence_after();
+                const uint32_t base = tmem + lane_base + b * 256 + half * 128;
+#pragma unroll
+                for (int c = 0; c < 128; c += 16) {
+                    uint32_t v0[16];
+                    tmem_ld_x16(base + c, v0);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) acc[c + j] += __uint_as_float(v0[j]);
+                }
+                tc_fence_before();
+                mbar_arrive(&acce[b]);
+                ++np;
+                if (++part == parts_per_tile) {
+                    int tm, tn;
+                    tile_coords(t_prom, p, tm, tn);
+                    const int row = tm * BM + quad * 32 + lane;
+                    if (row < p.M) {
+                        float *crow = p.C + int64_t(row) * p.ldc;
+                        const int col0 = tn * BN + half * 128;
+#pragma unroll
+                        for (int j = 0; j < 128; j += 4) {
+                            const int col = col0 + j;
+                            if (p.c_vec && col + 3 < p.N) {
+                                *reinterpret_cast<float4 *>(crow + col) =
+                                    make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 4; ++e)
+                                    if (col + e < p.N) crow[col + e] = acc[j + e];
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+                    part = 0;
+                    t_prom += gridDim.x;
+                }
+            }
+        };
+
+        int s = 0;
+        uint32_t ph = 0;
+        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            for (int kb = 0; kb < p.k_blocks; ++kb) {
+                mbar_wait(&full[s], ph);
+                const float4 *src = reinterpret_cast<const float4 *>(stages + s * STAGE_BYTES);
+                float4 *dst = reinterpret_cast<float4 *>(stages + s * STAGE_BYTES + RAW_BYTES);
+#pragma unroll 3
+                for (int i = 0; i < int(RAW_BYTES / 16) / COMBO_THREADS; ++i) {
+                    float4 v = src[ctid + i * COMBO_THREADS];
+                    v.x = tf32_small(v.x);
+                    v.y = tf32_small(v.y);
+                    v.z = tf32_small(v.z);
+                    v.w = tf32_small(v.w);
+                    dst[ctid + i * COMBO_THREADS] = v;
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ready[s]);
+                if (++s == STAGES) { s = 0; ph ^= 1; }
+                promote_ready(false);
+            }
+        }
+        promote_ready(true);
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+template <bool AMN, bool BMN>
+static cudaError_t launch_t(const CUtensorMap &ta, const CUtensorMap &tb, const Params &prm, int grid,
+                            cudaStream_t s) {
+    auto kern = gemm_3xtf32_kernel<AMN, BMN>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(SMEM_BYTES));
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    kern<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, prm);
+    return cudaGetLastError();
+}
+
+}  // namespace tf32
+
+bool tf32_available() { return true; }
+bool tf32_supported(const Problem &) { return true; }
+
+cudaError_t launch_3xtf32(const Problem &p, const Knobs &kn, cudaStream_t s) {
+    using namespace tf32;
+    const bool AMN = (p.la == 1);   // column-major A: M contiguous
+    const bool BMN = (p.lb == 0);   // row-major B: N contiguous
+    CUtensorMap ta, tb;
+    cudaError_t e;
+    if (AMN) e = make_tmap_2d(&ta, p.A, p.M, p.K, p.lda, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    else     e = make_tmap_2d(&ta, p.A, p.K, p.M, p.lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (e != cudaSuccess) return e;
+    if (BMN) e = make_tmap_2d(&tb, p.B, p.N, p.K, p.ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    else     e = make_tmap_2d(&tb, p.B, p.K, p.N, p.ldb, BK, BN, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (e != cudaSuccess) return e;
+
+    Params prm;
+    prm.M = p.M; prm.N = p.N; prm.K = p.K;
+    prm.C = p.C; prm.ldc = p.ldc;
+    prm.tiles_m = (p.M + BM - 1) / BM;
+    prm.tiles_n = (p.N + BN - 1) / BN;
+    prm.num_tiles = prm.tiles_m * prm.tiles_n;
+    prm.k_blocks = (p.K + BK - 1) / BK;
+    prm.group = kn.raster_group > 0 ? kn.raster_group : 16;
+    prm.promote = kn.promote_kblocks > 0 ? kn.promote_kblocks : 8;   // 128 of K per TMEM partial
+    prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
+    int grid = kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms;
+    if (grid > prm.num_tiles) grid = prm.num_tiles;
+    if (grid < 1) grid = 1;
+
+    if (AMN && BMN)  return launch_t<true, true>(ta, tb, prm, grid, s);
+    if (AMN && !BMN) return launch_t<true, false>(ta, tb, prm, grid, s);
+    if (!AMN && BMN) return launch_t<false, true>(ta, tb, prm, grid, s);
+    return launch_t<false, false>(ta, tb, prm, grid, s);
+}
+
 }  // namespace lpy

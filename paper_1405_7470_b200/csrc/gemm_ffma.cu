@@ -255,11 +255,11 @@ cudaError_t launch_ffma(const Problem &p, const Knobs &kn, cudaStream_t s) {
     const bool BKM = (p.lb == 1);  // column-major B: K contiguous
     CUtensorMap ta, tb;
     cudaError_t e;
-    if (AK) e = make_tmap_2d(&ta, p.A, p.K, p.M, p.lda, BK, BM, true);
-    else    e = make_tmap_2d(&ta, p.A, p.M, p.K, p.lda, BM, BK, false);
+    if (AK) e = make_tmap_2d(&ta, p.A, p.K, p.M, p.lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+    else    e = make_tmap_2d(&ta, p.A, p.M, p.K, p.lda, BM, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
     if (e != cudaSuccess) return e;
-    if (BKM) e = make_tmap_2d(&tb, p.B, p.K, p.N, p.ldb, BK, BN, true);
-    else     e = make_tmap_2d(&tb, p.B, p.N, p.K, p.ldb, BN, BK, false);
+    if (BKM) e = make_tmap_2d(&tb, p.B, p.K, p.N, p.ldb, BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    else     e = make_tmap_2d(&tb, p.B, p.N, p.K, p.ldb, BN, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
     if (e != cudaSuccess) return e;
 
     Params prm;

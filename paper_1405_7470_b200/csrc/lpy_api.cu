@@ -103,6 +103,17 @@ lpy_status device_info(DeviceInfo &out) {
     return LPY_OK;
 }
 
+// Copy `lines` lines of `inner` floats between pitched buffers; one linear DMA
+// when both sides are packed (2-D copies of very tall matrices run far below
+// PCIe bandwidth).
+cudaError_t copy_lines(void *dst, int64_t ld_dst, const void *src, int64_t ld_src, int64_t inner,
+                       int64_t lines, cudaMemcpyKind kind, cudaStream_t s) {
+    if (ld_dst == inner && ld_src == inner)
+        return cudaMemcpyAsync(dst, src, size_t(inner * lines) * 4, kind, s);
+    return cudaMemcpy2DAsync(dst, size_t(ld_dst) * 4, src, size_t(ld_src) * 4, size_t(inner) * 4,
+                             size_t(lines), kind, s);
+}
+
 lpy_path resolve_path(int64_t M, int64_t N, int64_t K, lpy_path requested) {
     if (requested != LPY_PATH_AUTO) return requested;
     // 3xTF32 on the tensor cores wins once there is enough work to fill the
@@ -134,7 +145,7 @@ static PFN_encodeTiled get_encode() {
 }
 
 cudaError_t make_tmap_2d(CUtensorMap *tm, const float *base, uint64_t inner, uint64_t outer, uint64_t ld,
-                         uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
+                         uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swizzle) {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
     cuuint64_t dims[2] = {inner, outer};
@@ -143,7 +154,7 @@ cudaError_t make_tmap_2d(CUtensorMap *tm, const float *base, uint64_t inner, uin
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box,
                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                     swizzle,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -280,15 +291,13 @@ lpy_status lpy_gemm_f32_host(int64_t M, int64_t N, int64_t K, const float *A, in
         if (o.extent() == 0) continue;
         e = cudaMallocAsync(reinterpret_cast<void **>(&dev_buf[i]), size_t(o.lines() * dev_ld[i]) * 4, s);
         if (e == cudaSuccess && i < 2)
-            e = cudaMemcpy2DAsync(dev_buf[i], size_t(dev_ld[i]) * 4, o.p, size_t(o.ld) * 4,
-                                  size_t(o.inner()) * 4, size_t(o.lines()), cudaMemcpyHostToDevice, s);
+            e = copy_lines(dev_buf[i], dev_ld[i], o.p, o.ld, o.inner(), o.lines(), cudaMemcpyHostToDevice, s);
     }
     if (e == cudaSuccess) {
         st = lpy_gemm_f32_ex(M, N, K, dev_buf[0], dev_ld[0], layout_a, dev_buf[1], dev_ld[1], layout_b,
                              dev_buf[2], dev_ld[2], layout_c, stream, path, nullptr);
         if (st == LPY_OK)
-            e = cudaMemcpy2DAsync(C, size_t(ldc) * 4, dev_buf[2], size_t(dev_ld[2]) * 4,
-                                  size_t(oc.inner()) * 4, size_t(oc.lines()), cudaMemcpyDeviceToHost, s);
+            e = copy_lines(C, ldc, dev_buf[2], dev_ld[2], oc.inner(), oc.lines(), cudaMemcpyDeviceToHost, s);
     }
     for (int i = 0; i < 3; ++i)
         if (dev_buf[i]) cudaFreeAsync(dev_buf[i], s);

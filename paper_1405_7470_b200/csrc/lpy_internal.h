@@ -31,9 +31,9 @@ struct Knobs {
 
 // 2-D tensor map over a strided matrix: `inner` contiguous elements per line,
 // `outer` lines at stride `ld` elements; box = box_inner x box_outer elements.
-// swizzle128 selects CU_TENSOR_MAP_SWIZZLE_128B (else none).
+// `swizzle` is the smem swizzle mode TMA applies to the box.
 cudaError_t make_tmap_2d(CUtensorMap *tm, const float *base, uint64_t inner, uint64_t outer,
-                         uint64_t ld, uint32_t box_inner, uint32_t box_outer, bool swizzle128);
+                         uint64_t ld, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swizzle);
 
 cudaError_t launch_ffma(const Problem &p, const Knobs &k, cudaStream_t s);
 cudaError_t launch_3xtf32(const Problem &p, const Knobs &k, cudaStream_t s);

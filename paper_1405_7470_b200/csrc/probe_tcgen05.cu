@@ -1,13 +1,12 @@
 // Hardware probes for the 3xTF32 design (test/diagnostic library
 // liblpy_probe.so, not part of the product C-ABI):
 //   * lpy_probe_umma_tf32: one 128 x N tile D = A B^T through tcgen05.mma
-//     kind::tf32 with operands staged in shared memory in the exact canonical
-//     layouts the GEMM kernel uses (K-major SW128 or MN-major SW128, 32-wide
-//     k panels).  Verifies descriptor encodings and measures how the tensor
-//     core treats fp32 operand bits (truncate vs round) and how it rounds the
-//     accumulation (reading A10).
-//   * lpy_probe_umma_rate: back-to-back kind::tf32 MMAs to measure cycles per
-//     instruction (the TF32 tensor roofline per SM).
+//     kind::tf32 with operands staged in shared memory in the canonical layouts
+//     the GEMM kernels use.  Verifies descriptor encodings and measures how the
+//     tensor core treats fp32 operand bits (truncate vs round) and how it rounds
+//     the accumulation (readings A9, A10).
+//   * lpy_probe_umma_rate: back-to-back kind::tf32 MMAs (cycles per instruction).
+//   * lpy_probe_ffma_rate: FP32 FMA pipe throughput (FFMA and packed FFMA2).
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "ptx.cuh"
@@ -15,36 +14,45 @@
 namespace lpy {
 namespace probe {
 
-// Byte offset of element (r, k) of an R x Kp operand tile in the canonical
-// layouts used by the GEMM: 32-wide k panels of R*128 bytes each.
-__device__ __forceinline__ uint32_t kmajor_off(int r, int k, int R) {
-    const int p = k >> 5, kk = k & 31;
-    return p * R * 128 + r * 128 + ((((kk >> 2) ^ (r & 7))) << 4) + (kk & 3) * 4;
-}
-__device__ __forceinline__ uint32_t mnmajor_off(int r, int k, int R) {
-    const int p = k >> 5, kk = k & 31, b = r >> 5, rr = r & 31;
-    return p * R * 128 + b * 4096 + (kk >> 3) * 1024 + (kk & 7) * 128 +
-           ((((rr >> 2) ^ (kk & 7))) << 4) + (rr & 3) * 4;
+// Operand formats (R rows of the operand, k runs along Kp):
+//  0: K-major, 128B swizzle, 32-wide k panels   (rows of 128 B; SBO 1024)
+//  1: MN-major, 128B_BASE32B, 32-wide k panels  (32-row MN blocks of 32 k-rows x 128 B)
+//  2: K-major, 64B swizzle, 16-wide k panels    (rows of 64 B; SBO 512)
+//  3: MN-major, 128B_BASE32B, 16-wide k panels  (32-row MN blocks of 16 k-rows x 128 B)
+__device__ __forceinline__ uint32_t offset(int fmt, int r, int k, int R) {
+    switch (fmt) {
+        case 0: {
+            const int p = k >> 5, kk = k & 31;
+            return p * R * 128 + r * 128 + (((kk >> 2) ^ (r & 7)) << 4) + (kk & 3) * 4;
+        }
+        case 1: {
+            const int p = k >> 5, kk = k & 31, rr = r & 31;
+            return p * R * 128 + (r >> 5) * 4096 + kk * 128 + (((rr >> 3) ^ (kk & 3)) << 5) + (rr & 7) * 4;
+        }
+        case 2: {
+            const int p = k >> 4, kk = k & 15;
+            return p * R * 64 + r * 64 + (((kk >> 2) ^ ((r >> 1) & 3)) << 4) + (kk & 3) * 4;
+        }
+        default: {
+            const int p = k >> 4, kk = k & 15, rr = r & 31;
+            return p * R * 64 + (r >> 5) * 2048 + kk * 128 + (((rr >> 3) ^ (kk & 3)) << 5) + (rr & 7) * 4;
+        }
+    }
 }
 
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= uint64_t((saddr >> 4) & 0x3FFF);
-    d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
-    d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
-    d |= uint64_t(1) << 46;                 // version (sm100)
-    d |= uint64_t(2) << 61;                 // SWIZZLE_128B
-    return d;
-}
-
-__device__ __forceinline__ uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
-           (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+// Descriptor of k-slice q (8 elements) for format fmt.
+__device__ __forceinline__ uint64_t desc(int fmt, uint32_t base, int q, int R) {
+    switch (fmt) {
+        case 0: return umma_sdesc(base + (q >> 2) * R * 128 + (q & 3) * 32, 16, 1024, 2);
+        case 1: return umma_sdesc(base + (q >> 2) * R * 128 + (q & 3) * 1024, 4096, 512, 1);
+        case 2: return umma_sdesc(base + (q >> 1) * R * 64 + (q & 1) * 32, 16, 512, 4);
+        default: return umma_sdesc(base + (q >> 1) * R * 64 + (q & 1) * 1024, 2048, 512, 1);
+    }
 }
 
 // 128 threads.  A: 128 x Kp row-major (A(m,k)), B: N x Kp row-major (B(n,k)).
-__global__ void umma_tile_kernel(const float *A, const float *B, float *D, int N, int Kp, int a_mn,
-                                 int b_mn, int accumulate_first) {
+__global__ void umma_tile_kernel(const float *A, const float *B, float *D, int N, int Kp, int fa,
+                                 int fb, int accumulate_first) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t *base = smem_raw + (((raw + 1023) & ~1023u) - raw);
@@ -53,16 +61,10 @@ __global__ void umma_tile_kernel(const float *A, const float *B, float *D, int N
     __shared__ uint64_t bar;
     __shared__ uint32_t tmem_base;
 
-    for (int idx = threadIdx.x; idx < 128 * Kp; idx += blockDim.x) {
-        const int r = idx / Kp, k = idx % Kp;
-        const uint32_t off = a_mn ? mnmajor_off(r, k, 128) : kmajor_off(r, k, 128);
-        *reinterpret_cast<float *>(sa + off) = A[idx];
-    }
-    for (int idx = threadIdx.x; idx < N * Kp; idx += blockDim.x) {
-        const int r = idx / Kp, k = idx % Kp;
-        const uint32_t off = b_mn ? mnmajor_off(r, k, N) : kmajor_off(r, k, N);
-        *reinterpret_cast<float *>(sb + off) = B[idx];
-    }
+    for (int idx = threadIdx.x; idx < 128 * Kp; idx += blockDim.x)
+        *reinterpret_cast<float *>(sa + offset(fa, idx / Kp, idx % Kp, 128)) = A[idx];
+    for (int idx = threadIdx.x; idx < N * Kp; idx += blockDim.x)
+        *reinterpret_cast<float *>(sb + offset(fb, idx / Kp, idx % Kp, N)) = B[idx];
     fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the tensor core
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
@@ -78,16 +80,10 @@ __global__ void umma_tile_kernel(const float *A, const float *B, float *D, int N
     const uint32_t tmem = tmem_base;
 
     if (threadIdx.x == 0) {
-        const uint32_t idesc = idesc_tf32(128, N, a_mn, b_mn);
-        for (int q = 0; q < Kp / 8; ++q) {
-            const int p = q >> 2, sub = q & 3;
-            uint64_t da, db;
-            if (a_mn) da = sdesc(smem_u32(sa) + p * 128 * 128 + sub * 1024, 4096, 1024);
-            else      da = sdesc(smem_u32(sa) + p * 128 * 128 + sub * 32, 16, 1024);
-            if (b_mn) db = sdesc(smem_u32(sb) + p * N * 128 + sub * 1024, 4096, 1024);
-            else      db = sdesc(smem_u32(sb) + p * N * 128 + sub * 32, 16, 1024);
-            umma_tf32(tmem, da, db, idesc, (q > 0 || accumulate_first) ? 1u : 0u);
-        }
+        const uint32_t idesc = umma_idesc_tf32(128, N, fa & 1, fb & 1);
+        for (int q = 0; q < Kp / 8; ++q)
+            umma_tf32(tmem, desc(fa, smem_u32(sa), q, 128), desc(fb, smem_u32(sb), q, N), idesc,
+                      (q > 0 || accumulate_first) ? 1u : 0u);
         umma_commit(&bar);
     }
     __syncwarp();
@@ -96,14 +92,11 @@ __global__ void umma_tile_kernel(const float *A, const float *B, float *D, int N
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int row = warp * 32 + lane;
-    for (int c0 = 0; c0 < N; c0 += 8) {
-        uint32_t v[8];
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                       "=r"(v[6]), "=r"(v[7])
-                     : "r"(tmem + (uint32_t(warp * 32) << 16) + c0));
+    for (int c0 = 0; c0 < N; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld_x16(tmem + (uint32_t(warp * 32) << 16) + c0, v);
         tmem_ld_wait();
-        for (int j = 0; j < 8; ++j) D[row * N + c0 + j] = __uint_as_float(v[j]);
+        for (int j = 0; j < 16; ++j) D[row * N + c0 + j] = __uint_as_float(v[j]);
     }
     tc_fence_before();
     __syncthreads();
@@ -131,9 +124,9 @@ __global__ void umma_rate_kernel(int N, int iters, long long *cycles) {
     __syncthreads();
     tc_fence_after();
     if (threadIdx.x == 0) {
-        const uint32_t idesc = idesc_tf32(128, N, 0, 0);
-        const uint64_t da = sdesc(smem_u32(base), 16, 1024);
-        const uint64_t db = sdesc(smem_u32(base) + 128 * 128, 16, 1024);
+        const uint32_t idesc = umma_idesc_tf32(128, N, 0, 0);
+        const uint64_t da = umma_sdesc(smem_u32(base), 16, 1024, 2);
+        const uint64_t db = umma_sdesc(smem_u32(base) + 128 * 128, 16, 1024, 2);
         long long t0 = clock64();
         for (int i = 0; i < iters; ++i) umma_tf32(tmem_base, da, db, idesc, i > 0 ? 1u : 0u);
         umma_commit(&bar);
@@ -146,36 +139,6 @@ __global__ void umma_rate_kernel(int N, int iters, long long *cycles) {
     if (threadIdx.x < 32) tmem_dealloc(tmem_base, 256);
 }
 
-}  // namespace probe
-}  // namespace lpy
-
-extern "C" {
-
-int lpy_probe_umma_tf32(const float *A, const float *B, float *D, int N, int Kp, int a_mn, int b_mn,
-                        int accumulate_first, void *stream) {
-    if (N < 16 || N > 256 || N % 16 || Kp < 8 || Kp > 64 || Kp % 32) return 1;
-    const size_t smem = 1024 + size_t(128 + N) * Kp * 4;
-    cudaFuncSetAttribute(lpy::probe::umma_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    lpy::probe::umma_tile_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(
-        A, B, D, N, Kp, a_mn, b_mn, accumulate_first);
-    return int(cudaGetLastError());
-}
-
-int lpy_probe_umma_rate(int N, int iters, int ctas, long long *cycles_dev, void *stream) {
-    const size_t smem = 1024 + size_t(128 + 256) * 32 * 4;
-    cudaFuncSetAttribute(lpy::probe::umma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    lpy::probe::umma_rate_kernel<<<ctas, 128, smem, static_cast<cudaStream_t>(stream)>>>(N, iters,
-                                                                                         cycles_dev);
-    return int(cudaGetLastError());
-}
-
-}  // extern "C"
-
-// ---------------------------------------------------------------- FFMA pipe rate
-namespace lpy {
-namespace probe {
 __global__ void ffma_rate_kernel(float *out, int iters, float x, float y) {
     float a[16];
 #pragma unroll
@@ -189,6 +152,7 @@ __global__ void ffma_rate_kernel(float *out, int iters, float x, float y) {
     for (int j = 0; j < 16; ++j) s += a[j];
     if (s == 12345.678f) out[0] = s;   // keep the work alive
 }
+
 __global__ void ffma2_rate_kernel(float *out, int iters, float x, float y) {
     uint64_t a[8];
     uint64_t xx, yy;
@@ -212,13 +176,42 @@ __global__ void ffma2_rate_kernel(float *out, int iters, float x, float y) {
     }
     if (s == 12345.678f) out[0] = s;
 }
+
 }  // namespace probe
 }  // namespace lpy
 
-extern "C" int lpy_probe_ffma_rate(float *out, int iters, int blocks, int threads, int pair, void *stream) {
-    if (pair)
-        lpy::probe::ffma2_rate_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(out, iters, 0.999f, 0.001f);
-    else
-        lpy::probe::ffma_rate_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(out, iters, 0.999f, 0.001f);
+extern "C" {
+
+int lpy_probe_umma_tf32(const float *A, const float *B, float *D, int N, int Kp, int fa, int fb,
+                        int accumulate_first, void *stream) {
+    if (N < 16 || N > 256 || N % 16 || Kp < 32 || Kp > 64 || Kp % 32 || fa < 0 || fa > 3 || fb < 0 ||
+        fb > 3)
+        return 1;
+    if (((fa & 1) || (fb & 1)) && N % 32) return 1;
+    const size_t smem = 1024 + size_t(128 + N) * Kp * 4;
+    cudaFuncSetAttribute(lpy::probe::umma_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    lpy::probe::umma_tile_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(
+        A, B, D, N, Kp, fa, fb, accumulate_first);
     return int(cudaGetLastError());
 }
+
+int lpy_probe_umma_rate(int N, int iters, int ctas, long long *cycles_dev, void *stream) {
+    const size_t smem = 1024 + size_t(128 + 256) * 32 * 4;
+    cudaFuncSetAttribute(lpy::probe::umma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    lpy::probe::umma_rate_kernel<<<ctas, 128, smem, static_cast<cudaStream_t>(stream)>>>(N, iters,
+                                                                                         cycles_dev);
+    return int(cudaGetLastError());
+}
+
+int lpy_probe_ffma_rate(float *out, int iters, int blocks, int threads, int pair, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (pair)
+        lpy::probe::ffma2_rate_kernel<<<blocks, threads, 0, s>>>(out, iters, 0.999f, 0.001f);
+    else
+        lpy::probe::ffma_rate_kernel<<<blocks, threads, 0, s>>>(out, iters, 0.999f, 0.001f);
+    return int(cudaGetLastError());
+}
+
+}  // extern "C"

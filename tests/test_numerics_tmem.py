@@ -45,10 +45,12 @@ def tile(probe, A, B, a_mn=0, b_mn=0, acc_first=0):
     return dD.cpu().numpy()
 
 
-@pytest.mark.parametrize("a_mn", [0, 1])
-@pytest.mark.parametrize("b_mn", [0, 1])
+@pytest.mark.parametrize("a_mn", [0, 1, 2, 3])
+@pytest.mark.parametrize("b_mn", [0, 1, 2, 3])
 @pytest.mark.parametrize("N,Kp", [(64, 32), (256, 32), (128, 64), (224, 64)])
 def test_descriptors_exact_on_tf32_values(probe, a_mn, b_mn, N, Kp):
+    """Operand formats: 0 K-major SW128, 1 MN-major 128B_BASE32B (32-k panels),
+    2 K-major SW64, 3 MN-major 128B_BASE32B (16-k panels)."""
     rng = np.random.default_rng(N + Kp)
     A = rng.integers(-8, 9, (128, Kp)).astype(np.float32) * np.float32(0.25)
     B = rng.integers(-8, 9, (N, Kp)).astype(np.float32)
