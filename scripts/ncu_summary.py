@@ -1,0 +1,67 @@
+#!/usr/bin/env python
+"""Summarise an ncu report (.ncu-rep) into the handful of metrics DESIGN.md and
+bench.py's roofline block cite: duration, DRAM traffic, tensor / FMA pipe
+utilisation, shared-memory wavefronts, registers, occupancy, SM clock.
+
+usage: python scripts/ncu_summary.py gpurun_out/prof_3xtf32.ncu-rep [> profiles/…txt]
+"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum",
+    "sm__cycles_elapsed.avg.per_second",
+    "dram__bytes_read.sum",
+    "dram__bytes_write.sum",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_bytes.sum",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed.avg.per_cycle_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
+    "launch__registers_per_thread",
+    "launch__grid_size",
+    "launch__block_size",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "smsp__average_warp_latency_issue_stalled_barrier",
+]
+
+
+def main(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    for vals in rows[2:]:
+        name = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
+        print(f"kernel: {name}")
+        for k in KEYS:
+            for i, h in enumerate(hdr):
+                if h == k or h.endswith("." + k) or h.split(".", 1)[-1] == k:
+                    print(f"  {k:85s} {vals[i]:>16s} {units[i]}")
+                    break
+        # stall reasons (warp-state sampling), top 8
+        stalls = []
+        for i, h in enumerate(hdr):
+            if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio"):
+                try:
+                    stalls.append((float(vals[i]), h[len("smsp__average_warps_issue_stalled_"):-len(
+                        "_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
+        if stalls:
+            print("  top stall reasons (warps per issue-active cycle):")
+            for v, n in sorted(stalls, reverse=True)[:8]:
+                print(f"    {n:40s} {v:8.3f}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
