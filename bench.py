@@ -65,6 +65,26 @@ def roofline_peak(path: str):
     return "alu", 148 * 128 * 2 * mhz * 1e6 / 1e12, f"148 SM x 128 FP32 lanes x 2 x {mhz} MHz ({src} clock)"
 
 
+def profile_traffic(path: str, n: int):
+    """DRAM bytes (read + write) per launch of `path`'s kernel at size n from the
+    newest committed `ncu --set full` summary (profiles/rNN_ncu_full_<path>_n<n>.txt),
+    or (None, None)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_full_{path}_n{n}.txt")))
+    if not files:
+        return None, None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    total = 0.0
+    seen = 0
+    with open(files[-1]) as f:
+        for line in f:
+            parts = line.split()
+            if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum") and len(parts) >= 3:
+                total += float(parts[1]) * scale.get(parts[2], 1)
+                seen += 1
+    return (int(total), os.path.relpath(files[-1], ROOT)) if seen == 2 else (None, None)
+
+
 class ClockSampler:
     """Samples SM clock + throttle reasons with `nvidia-smi -lms` during the
     timed region (the profiling guide's clocks line)."""
@@ -387,8 +407,10 @@ def main():
                 return {"bound": bound, "achieved": None, "peak": peak, "unit": "TFLOP/s",
                         "frac": None, "traffic": None, "peak_note": note}
             achieved = flops / (kms * 1e-3) / 1e12
+            traffic, tsrc = profile_traffic(path, n)
             return {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3),
-                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "traffic_source": tsrc, "algorithmic_bytes": 4 * 3 * n * n,
                     "peak_note": note, "kernel_ms_mean": round(kms, 4)}
 
         cpu = None
