@@ -4,49 +4,58 @@
 // Split precision (readings A9/A10).  The tensor core reads an fp32
 // operand as tf32 by TRUNCATING its low 13 mantissa bits (measured:
 // tests/test_numerics_tmem.py).  So each fp32 x is used as
-//     big   = x                      (the hardware sees trunc_tf32(x))
-//     small = rna_tf32(x - trunc_tf32(x))   (computed here, exact residual rounded)
+//     big   = x                                  (the hardware sees trunc_tf32(x))
+//     small = rna_tf32(x - trunc_tf32(x))        (computed here; exact residual, rounded)
 // and  a*b ~= a_big*b_small + a_small*b_big + a_big*b_big  (small*small dropped;
 // the small terms go first).  Per product the representation error is below
 // 2^-20 |a||b|.  TMEM accumulation rounds toward zero (measured), so the
-// accumulator is PROMOTED: every `promote` k-blocks the MMA warp closes a TMEM
-// partial (double-buffered, 2 x 256 columns) and the epilogue warps add it into
-// fp32 registers with round-to-nearest.
+// accumulator is PROMOTED: every `promote` k-blocks the MMA thread closes a TMEM
+// partial (double-buffered, 2 x 256 columns) and the partial is added into fp32
+// registers with round-to-nearest.
 //
 // Schedule (Loo.py's split_iname / group-local tags / add_prefetch / precompute,
-// P:499-632, realised the Blackwell way):
-//   * persistent CTAs over 128 x 256 output tiles in grouped raster order;
-//   * warp 0 (one lane): TMA producer, A[128 x 16] + B[16 x 256] fp32 per
-//     k-block into a 4-stage ring ("add_prefetch");
-//   * warps 2-3: split transform, raw stage -> small stage in the same swizzled
-//     layout (an elementwise "precompute" into local memory), then
-//     fence.proxy.async so the tensor core sees it;
-//   * warp 1 (one lane): tcgen05.mma kind::tf32 M=128 N=256 K=8, three per
-//     k-slice, accumulating in TMEM; tcgen05.commit frees the stage and
-//     publishes each partial;
-//   * warps 4-11: promotion + epilogue; each owns 32 TMEM lanes (rows) x 128
-//     columns, accumulates partials in registers, and stores the finished row
-//     segment with predicated 16-byte stores (ragged M/N edges; TMA zero-fill
-//     covers ragged K).
+// P:499-632, realised the Blackwell way).  CG = 1: one CTA per 128 x 256 output
+// tile.  CG = 2: a CTA pair (thread-block cluster of 2 on one TPC) per 256 x 256
+// tile with tcgen05.mma.cta_group::2 -- each CTA stages its own 128 rows of A and
+// its own 128 columns of B, the leader issues M=256 N=256 MMAs that read both
+// CTAs' shared memory, and each CTA's TMEM receives its 128 rows.  That halves
+// the per-SM shared-memory traffic for B, the bound of the CG = 1 kernel.
+// Roles (per CTA, persistent over tiles in grouped raster order):
+//   * warp 0 (one lane): TMA producer, A[128 x 16] + B[16 x 256/CG] fp32 per
+//     k-block into the stage ring ("add_prefetch");
+//   * warp 1 (one lane, leader CTA): tcgen05.mma issuer, three kind::tf32 MMAs
+//     per k-slice of 8; tcgen05.commit frees the stage (multicast to both CTAs
+//     for CG = 2) and publishes each finished TMEM partial;
+//   * warps 2-9: split transform of every stage (raw -> small in the same
+//     swizzled layout, then fence.proxy.async and an arrive on the leader's
+//     "ready" barrier) and, between stages, promotion of finished partials into
+//     128 register accumulators per thread and the store of finished tiles
+//     (predicated 16-byte stores: ragged M/N; TMA zero-fill covers ragged K).
 // Operand smem layouts: K-major tiles use the 64B swizzle (16 fp32 per row);
 // MN-major tf32 tiles must use SWIZZLE_128B_BASE32B (TMA "128B_ATOM_32B").
+#include <cstdlib>
 #include "lpy_internal.h"
 #include "ptx.cuh"
 
 namespace lpy {
 namespace tf32 {
 
-constexpr int BM = 128, BN = 256, BK = 16;
-constexpr int STAGES = 4;
-constexpr int THREADS = 320;            // 10 warps
-constexpr int COMBO_THREADS = 256;      // warps 2-9: transform + promotion + epilogue
+constexpr int BM = 128, BN = 256, BK = 16;   // BM rows per CTA; BN columns per tile
+constexpr int THREADS = 320;                 // 10 warps
+constexpr int COMBO_THREADS = 256;           // warps 2-9: transform + promotion + epilogue
 constexpr int COMBO_WARPS = COMBO_THREADS / 32;
-constexpr uint32_t A_BYTES = BM * BK * 4;            // 8 KB
-constexpr uint32_t B_BYTES = BN * BK * 4;            // 16 KB
-constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;    // 24 KB (TMA transaction per stage)
-constexpr uint32_t STAGE_BYTES = 2 * RAW_BYTES;      // raw + small
-constexpr uint32_t TMEM_COLS = 512;                  // 2 partial buffers x 256 columns
-constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * STAGE_BYTES + 256;
+constexpr uint32_t TMEM_COLS = 512;          // 2 partial buffers x 256 columns
+
+template <int CG>
+struct Cfg {
+    static constexpr int BN_CTA = BN / CG;                       // B columns staged per CTA
+    static constexpr int STAGES = CG == 2 ? 6 : 4;
+    static constexpr uint32_t A_BYTES = BM * BK * 4;             // 8 KB
+    static constexpr uint32_t B_BYTES = BN_CTA * BK * 4;         // 16 KB / CG
+    static constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;     // TMA transaction per stage
+    static constexpr uint32_t STAGE_BYTES = 2 * RAW_BYTES;       // raw + small
+    static constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * STAGE_BYTES + 256;
+};
 
 struct Params {
     int M, N, K;
@@ -86,42 +95,55 @@ __device__ __forceinline__ float tf32_small(float x) {
     return __uint_as_float((r + 0x1000u) & 0xFFFFE000u);
 }
 
-template <bool AMN, bool BMN>
+// Arrive (one per warp) on the leader CTA's copy of `bar`.
+template <int CG>
+__device__ __forceinline__ void arrive_leader(uint64_t *bar) {
+    if constexpr (CG == 1) mbar_arrive(bar);
+    else                   mbar_arrive_remote(mapa_shared(smem_u32(bar), 0));
+}
+
+template <int CG, bool AMN, bool BMN>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const Params p) {
+    using C_ = Cfg<CG>;
+    constexpr int STAGES = C_::STAGES;
+    constexpr uint32_t A_BYTES = C_::A_BYTES, RAW_BYTES = C_::RAW_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
+
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t *stages = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
     uint64_t *bars = reinterpret_cast<uint64_t *>(stages + STAGES * STAGE_BYTES);
-    uint64_t *full = bars;                  // TMA -> transform
-    uint64_t *ready = bars + STAGES;        // transform -> MMA
-    uint64_t *empty = bars + 2 * STAGES;    // MMA -> producer
-    uint64_t *accf = bars + 3 * STAGES;     // MMA -> epilogue (partial b complete)
-    uint64_t *acce = accf + 2;              // epilogue -> MMA (partial b drained)
+    uint64_t *full = bars;                  // TMA -> transform (per CTA)
+    uint64_t *ready = bars + STAGES;        // transforms of the pair -> MMA (leader)
+    uint64_t *empty = bars + 2 * STAGES;    // MMA commit -> producer (per CTA)
+    uint64_t *accf = bars + 3 * STAGES;     // MMA commit -> promotion (per CTA)
+    uint64_t *acce = accf + 2;              // promotions of the pair -> MMA (leader)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const int rank = CG == 2 ? int(cluster_ctarank()) : 0;
+    const int unit0 = blockIdx.x / CG, units = gridDim.x / CG;   // this pair's first tile, stride
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&ready[s], COMBO_WARPS);
+            mbar_init(&ready[s], CG * COMBO_WARPS);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&accf[b], 1);
-            mbar_init(&acce[b], COMBO_THREADS);
+            mbar_init(&acce[b], CG * COMBO_WARPS);
         }
         fence_mbar_init();
     }
     if (warp == 1) {
-        tmem_alloc(tmem_slot, TMEM_COLS);
-        tmem_relinquish();
+        tmem_alloc_cg<CG>(tmem_slot, TMEM_COLS);
+        tmem_relinquish_cg<CG>();
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const int parts_per_tile = (p.k_blocks + p.promote - 1) / p.promote;
@@ -133,10 +155,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             tma_prefetch_desc(&tmB);
             int s = 0;
             uint32_t ph = 0;
-            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            for (int t = unit0; t < p.num_tiles; t += units) {
                 int tm, tn;
                 tile_coords(t, p, tm, tn);
-                const int m0 = tm * BM, n0 = tn * BN;
+                const int m0 = tm * (BM * CG) + rank * BM;
+                const int n0 = tn * BN + rank * C_::BN_CTA;
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1);
                     uint8_t *sa = stages + s * STAGE_BYTES;
@@ -151,7 +174,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                     if constexpr (BMN) {
 #pragma unroll
-                        for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * 2048, &tmB, &full[s], n0 + 32 * j, k0);
+                        for (int j = 0; j < C_::BN_CTA / 32; ++j)
+                            tma_load_2d(sb + j * 2048, &tmB, &full[s], n0 + 32 * j, k0);
                     } else {
                         tma_load_2d(sb, &tmB, &full[s], k0, n0);
                     }
@@ -160,21 +184,21 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc_tf32(BM, BN, AMN ? 1 : 0, BMN ? 1 : 0);
+        // ------------------------------------------------ MMA issuer (leader CTA)
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = umma_idesc_tf32(BM * CG, BN, AMN ? 1 : 0, BMN ? 1 : 0);
             int s = 0;
             uint32_t ph = 0;
-            uint32_t npart = 0;   // partials issued by this CTA
-            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            uint32_t npart = 0;   // partials issued by this pair
+            for (int t = unit0; t < p.num_tiles; t += units) {
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     const bool first = (kb % p.promote) == 0;
                     const uint32_t b = npart & 1;
                     if (first) {
-                        mbar_wait(&acce[b], ((npart >> 1) & 1) ^ 1);   // buffer drained
+                        mbar_wait_cluster(&acce[b], ((npart >> 1) & 1) ^ 1);   // buffer drained (both CTAs)
                         tc_fence_after();
                     }
-                    mbar_wait(&ready[s], ph);
+                    mbar_wait_cluster(&ready[s], ph);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(stages + s * STAGE_BYTES);
                     const uint32_t sb = sa + A_BYTES;
@@ -184,14 +208,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const uint64_t a_big = op_desc<AMN>(sa, sub), b_big = op_desc<BMN>(sb, sub);
                         const uint64_t a_small = op_desc<AMN>(sa + RAW_BYTES, sub);
                         const uint64_t b_small = op_desc<BMN>(sb + RAW_BYTES, sub);
-                        umma_tf32(d, a_big, b_small, idesc, (first && sub == 0) ? 0u : 1u);
-                        umma_tf32(d, a_small, b_big, idesc, 1u);
-                        umma_tf32(d, a_big, b_big, idesc, 1u);
+                        umma_tf32_cg<CG>(d, a_big, b_small, idesc, (first && sub == 0) ? 0u : 1u);
+                        umma_tf32_cg<CG>(d, a_small, b_big, idesc, 1u);
+                        umma_tf32_cg<CG>(d, a_big, b_big, idesc, 1u);
                     }
-                    umma_commit(&empty[s]);
+                    umma_commit_cg<CG>(&empty[s]);
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                     if ((kb % p.promote) == p.promote - 1 || kb == p.k_blocks - 1) {
-                        umma_commit(&accf[b]);
+                        umma_commit_cg<CG>(&accf[b]);
                         ++npart;
                     }
                 }
@@ -203,7 +227,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // partial is complete, fold it into their fp32 register accumulators
         // (checked without blocking after each stage; the MMA only needs a
         // buffer back `promote` stages later).  After a tile's last partial
-        // they store its 128 x 256 block of C.
+        // they store this CTA's 128 x 256 block of C.
         const int ctid = threadIdx.x - 64;       // 0..255
         const int quad = warp & 3;               // TMEM lanes 32*quad .. +31 (hardware rule)
         const int half = (warp - 2) >> 2;        // columns 128*half .. +127
@@ -211,7 +235,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         float acc[128];
 #pragma unroll
         for (int j = 0; j < 128; ++j) acc[j] = 0.f;
-        int t_prom = blockIdx.x, part = 0;       // next partial to promote: (tile, part)
+        int t_prom = unit0, part = 0;            // next partial to promote: (tile, part)
         uint32_t np = 0;                         // partials promoted so far
 
         auto promote_ready = [&](bool block) {
@@ -234,12 +258,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int j = 0; j < 16; ++j) acc[c + j] += __uint_as_float(v0[j]);
                 }
                 tc_fence_before();
-                mbar_arrive(&acce[b]);
+                __syncwarp();
+                if (lane == 0) arrive_leader<CG>(&acce[b]);
                 ++np;
                 if (++part == parts_per_tile) {
                     int tm, tn;
                     tile_coords(t_prom, p, tm, tn);
-                    const int row = tm * BM + quad * 32 + lane;
+                    const int row = tm * (BM * CG) + rank * BM + quad * 32 + lane;
                     if (row < p.M) {
                         float *crow = p.C + int64_t(row) * p.ldc;
                         const int col0 = tn * BN + half * 128;
@@ -259,14 +284,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int j = 0; j < 128; ++j) acc[j] = 0.f;
                     part = 0;
-                    t_prom += gridDim.x;
+                    t_prom += units;
                 }
             }
         };
 
         int s = 0;
         uint32_t ph = 0;
-        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        for (int t = unit0; t < p.num_tiles; t += units) {
             for (int kb = 0; kb < p.k_blocks; ++kb) {
                 mbar_wait(&full[s], ph);
                 const float4 *src = reinterpret_cast<const float4 *>(stages + s * STAGE_BYTES);
@@ -282,7 +307,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&ready[s]);
+                if (lane == 0) arrive_leader<CG>(&ready[s]);
                 if (++s == STAGES) { s = 0; ph ^= 1; }
                 promote_ready(false);
             }
@@ -291,23 +316,69 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 
     tc_fence_before();
-    __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    if (warp == 1) tmem_dealloc_cg<CG>(tmem, TMEM_COLS);
 }
 
-template <bool AMN, bool BMN>
+template <int CG, bool AMN, bool BMN>
 static cudaError_t launch_t(const CUtensorMap &ta, const CUtensorMap &tb, const Params &prm, int grid,
                             cudaStream_t s) {
-    auto kern = gemm_3xtf32_kernel<AMN, BMN>;
+    auto kern = gemm_3xtf32_kernel<CG, AMN, BMN>;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(SMEM_BYTES));
+                                             int(Cfg<CG>::SMEM_BYTES));
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
-    kern<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, prm);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = Cfg<CG>::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, ta, tb, prm);
+}
+
+template <int CG>
+static cudaError_t launch_cg(const Problem &p, const Knobs &kn, cudaStream_t s) {
+    const bool AMN = (p.la == 1);   // column-major A: M contiguous
+    const bool BMN = (p.lb == 0);   // row-major B: N contiguous
+    constexpr int BN_CTA = Cfg<CG>::BN_CTA;
+    CUtensorMap ta, tb;
+    cudaError_t e;
+    if (AMN) e = make_tmap_2d(&ta, p.A, p.M, p.K, p.lda, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    else     e = make_tmap_2d(&ta, p.A, p.K, p.M, p.lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (e != cudaSuccess) return e;
+    if (BMN) e = make_tmap_2d(&tb, p.B, p.N, p.K, p.ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    else     e = make_tmap_2d(&tb, p.B, p.K, p.N, p.ldb, BK, BN_CTA, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (e != cudaSuccess) return e;
+
+    Params prm;
+    prm.M = p.M; prm.N = p.N; prm.K = p.K;
+    prm.C = p.C; prm.ldc = p.ldc;
+    prm.tiles_m = (p.M + BM * CG - 1) / (BM * CG);
+    prm.tiles_n = (p.N + BN - 1) / BN;
+    prm.num_tiles = prm.tiles_m * prm.tiles_n;
+    prm.k_blocks = (p.K + BK - 1) / BK;
+    prm.group = kn.raster_group > 0 ? kn.raster_group : 16 / CG;
+    prm.promote = kn.promote_kblocks > 0 ? kn.promote_kblocks : 8;   // 128 of K per TMEM partial
+    prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
+    int units = (kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms) / CG;  // CTAs (pairs) in the grid
+    if (units > prm.num_tiles) units = prm.num_tiles;
+    if (units < 1) units = 1;
+    const int grid = units * CG;
+
+    if (AMN && BMN)  return launch_t<CG, true, true>(ta, tb, prm, grid, s);
+    if (AMN && !BMN) return launch_t<CG, true, false>(ta, tb, prm, grid, s);
+    if (!AMN && BMN) return launch_t<CG, false, true>(ta, tb, prm, grid, s);
+    return launch_t<CG, false, false>(ta, tb, prm, grid, s);
 }
 
 }  // namespace tf32
@@ -316,36 +387,12 @@ bool tf32_available() { return true; }
 bool tf32_supported(const Problem &) { return true; }
 
 cudaError_t launch_3xtf32(const Problem &p, const Knobs &kn, cudaStream_t s) {
-    using namespace tf32;
-    const bool AMN = (p.la == 1);   // column-major A: M contiguous
-    const bool BMN = (p.lb == 0);   // row-major B: N contiguous
-    CUtensorMap ta, tb;
-    cudaError_t e;
-    if (AMN) e = make_tmap_2d(&ta, p.A, p.M, p.K, p.lda, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    else     e = make_tmap_2d(&ta, p.A, p.K, p.M, p.lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
-    if (e != cudaSuccess) return e;
-    if (BMN) e = make_tmap_2d(&tb, p.B, p.N, p.K, p.ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    else     e = make_tmap_2d(&tb, p.B, p.K, p.N, p.ldb, BK, BN, CU_TENSOR_MAP_SWIZZLE_64B);
-    if (e != cudaSuccess) return e;
-
-    Params prm;
-    prm.M = p.M; prm.N = p.N; prm.K = p.K;
-    prm.C = p.C; prm.ldc = p.ldc;
-    prm.tiles_m = (p.M + BM - 1) / BM;
-    prm.tiles_n = (p.N + BN - 1) / BN;
-    prm.num_tiles = prm.tiles_m * prm.tiles_n;
-    prm.k_blocks = (p.K + BK - 1) / BK;
-    prm.group = kn.raster_group > 0 ? kn.raster_group : 16;
-    prm.promote = kn.promote_kblocks > 0 ? kn.promote_kblocks : 8;   // 128 of K per TMEM partial
-    prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
-    int grid = kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms;
-    if (grid > prm.num_tiles) grid = prm.num_tiles;
-    if (grid < 1) grid = 1;
-
-    if (AMN && BMN)  return launch_t<true, true>(ta, tb, prm, grid, s);
-    if (AMN && !BMN) return launch_t<true, false>(ta, tb, prm, grid, s);
-    if (!AMN && BMN) return launch_t<false, true>(ta, tb, prm, grid, s);
-    return launch_t<false, false>(ta, tb, prm, grid, s);
+    // LPY_TF32_CG=1 selects the single-CTA variant (diagnostics / A-B comparison).
+    static const int cg = [] {
+        const char *e = getenv("LPY_TF32_CG");
+        return (e && e[0] == '1') ? 1 : 2;
+    }();
+    return cg == 1 ? tf32::launch_cg<1>(p, kn, s) : tf32::launch_cg<2>(p, kn, s);
 }
 
 }  // namespace lpy
