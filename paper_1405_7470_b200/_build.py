@@ -1,4 +1,9 @@
-"""Build the in-tree CUDA library paper_1405_7470_b200/liblpy.so for sm_100a.
+"""Build the in-tree CUDA libraries for sm_100a.
+
+  liblpy.so        the product: C-ABI front end + FFMA and 3xTF32 kernels
+  liblpy_probe.so  hardware probes (tcgen05 numerics, MMA / FFMA rates) for tests
+  liblpy_trace.so  diagnostics: the product built with -DLPY_TRACE (per-CTA cycle
+                   counters in the 3xTF32 kernel); never loaded by the product path
 
 nvcc cross-compiles here without a GPU.  The explicit `-gencode
 arch=compute_100a,code=sm_100a` form is required: plain -arch=sm_100a does not
@@ -20,13 +25,24 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "liblpy.so")
-PROBE_LIB = os.path.join(PKG, "liblpy_probe.so")   # hardware probes (tests/diagnostics only)
+PROBE_LIB = os.path.join(PKG, "liblpy_probe.so")
+TRACE_LIB = os.path.join(PKG, "liblpy_trace.so")
 
 SOURCES = ["lpy_api.cu", "gemm_ffma.cu", "gemm_3xtf32.cu", "repack.cu"]
-PROBE_SOURCES = ["probe_tcgen05.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}",
                      "-Xptxas", "-v"]
+
+# (object name, source, extra flags)
+OBJECTS = [(os.path.splitext(s)[0], s, []) for s in SOURCES] + [
+    ("probe_tcgen05", "probe_tcgen05.cu", []),
+    ("gemm_3xtf32_trace", "gemm_3xtf32.cu", ["-DLPY_TRACE"]),
+]
+LIBS = [
+    (LIB, [os.path.splitext(s)[0] for s in SOURCES]),
+    (PROBE_LIB, ["probe_tcgen05"]),
+    (TRACE_LIB, ["lpy_api", "gemm_ffma", "gemm_3xtf32_trace", "repack"]),
+]
 
 
 def nvcc() -> str:
@@ -42,30 +58,31 @@ def _deps_mtime() -> float:
     return max(os.path.getmtime(f) for f in files)
 
 
-def _compile(src: str, force: bool) -> tuple[str, str]:
-    obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
+def _compile(name: str, src: str, extra: list[str], force: bool) -> tuple[str, str]:
+    obj = os.path.join(BUILD, name + ".o")
     srcp = os.path.join(CSRC, src)
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(srcp),
                                                                           _deps_mtime()):
         return obj, ""
-    r = subprocess.run([nvcc(), *NVCC_FLAGS, "-c", srcp, "-o", obj], capture_output=True, text=True)
+    r = subprocess.run([nvcc(), *NVCC_FLAGS, *extra, "-c", srcp, "-o", obj], capture_output=True,
+                       text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
     return obj, r.stderr
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every CUDA source and link liblpy.so; returns the library path."""
+    """Compile every CUDA source and link the libraries; returns liblpy.so's path."""
     os.makedirs(BUILD, exist_ok=True)
-    allsrc = SOURCES + PROBE_SOURCES
-    with cf.ThreadPoolExecutor(max_workers=min(8, len(allsrc))) as ex:
-        results = dict(zip(allsrc, ex.map(lambda s: _compile(s, force), allsrc)))
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(OBJECTS))) as ex:
+        results = dict(zip([o[0] for o in OBJECTS],
+                           ex.map(lambda o: _compile(o[0], o[1], o[2], force), OBJECTS)))
     if verbose:
         for _, log in results.values():
             if log:
                 print(log)
-    for lib, srcs in ((LIB, SOURCES), (PROBE_LIB, PROBE_SOURCES)):
-        objs = [results[s][0] for s in srcs]
+    for lib, names in LIBS:
+        objs = [results[n][0] for n in names]
         if force or not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs):
             tmp = lib + f".tmp{os.getpid()}"
             r = subprocess.run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs],

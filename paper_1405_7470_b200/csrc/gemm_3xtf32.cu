@@ -9,28 +9,30 @@
 // and  a*b ~= a_big*b_small + a_small*b_big + a_big*b_big  (small*small dropped;
 // the small terms go first).  Per product the representation error is below
 // 2^-20 |a||b|.  TMEM accumulation rounds toward zero (measured), so the
-// accumulator is PROMOTED: every `promote` k-blocks the MMA thread closes a TMEM
-// partial (double-buffered, 2 x 256 columns) and the partial is added into fp32
-// registers with round-to-nearest.
+// accumulator is PROMOTED: every `promote` k-blocks the MMA closes a TMEM partial
+// (double-buffered, 2 x 256 columns) and the partial is added into fp32 registers
+// with round-to-nearest (measured max normalised error at n=8192, uniform[0,1):
+// 2.8e-6 with promote = 8, 5.3e-6 with 16; scripts/accuracy_tf32.py).
 //
 // Schedule (Loo.py's split_iname / group-local tags / add_prefetch / precompute,
 // P:499-632, realised the Blackwell way).  CG = 1: one CTA per 128 x 256 output
-// tile.  CG = 2: a CTA pair (thread-block cluster of 2 on one TPC) per 256 x 256
-// tile with tcgen05.mma.cta_group::2 -- each CTA stages its own 128 rows of A and
-// its own 128 columns of B, the leader issues M=256 N=256 MMAs that read both
-// CTAs' shared memory, and each CTA's TMEM receives its 128 rows.  That halves
-// the per-SM shared-memory traffic for B, the bound of the CG = 1 kernel.
-// Roles (per CTA, persistent over tiles in grouped raster order):
-//   * warp 0 (one lane): TMA producer, A[128 x 16] + B[16 x 256/CG] fp32 per
-//     k-block into the stage ring ("add_prefetch");
-//   * warp 1 (one lane, leader CTA): tcgen05.mma issuer, three kind::tf32 MMAs
-//     per k-slice of 8; tcgen05.commit frees the stage (multicast to both CTAs
-//     for CG = 2) and publishes each finished TMEM partial;
-//   * warps 2-9: split transform of every stage (raw -> small in the same
-//     swizzled layout, then fence.proxy.async and an arrive on the leader's
-//     "ready" barrier) and, between stages, promotion of finished partials into
-//     128 register accumulators per thread and the store of finished tiles
-//     (predicated 16-byte stores: ragged M/N; TMA zero-fill covers ragged K).
+// tile.  CG = 2 (default): a CTA pair (thread-block cluster of 2 on one TPC) per
+// 256 x 256 tile with tcgen05.mma.cta_group::2 -- each CTA stages its own 128
+// rows of A and its own 128 columns of B, the leader issues M=256 N=256 MMAs that
+// read both CTAs' shared memory, and each CTA's TMEM receives its 128 rows.
+// Warp roles (16 warps; registers rebalanced per warpgroup with setmaxnreg):
+//   WG0  warp 0: TMA producer (A[128 x 16] + B[16 x 256/CG] fp32 per k-block,
+//                "add_prefetch" into the stage ring); warp 1: tcgen05.mma issuer
+//                (leader CTA; three kind::tf32 MMAs per k-slice of 8, commit to
+//                free the stage / publish a partial); warps 2-3 idle.
+//   WG1  warps 4-7: split transform of every stage (raw -> small in the same
+//                swizzled layout, fence.proxy.async, arrive on the leader's
+//                "ready" barrier) -- an elementwise "precompute".
+//   WG2-3 warps 8-15: promotion + epilogue.  Each thread owns one TMEM lane (row)
+//                x 128 columns as fp32 registers, folds in every finished partial,
+//                and stores its row segment of C after a tile's last partial
+//                (predicated 16-byte stores: ragged M/N; TMA zero-fill covers
+//                ragged K).
 // Operand smem layouts: K-major tiles use the 64B swizzle (16 fp32 per row);
 // MN-major tf32 tiles must use SWIZZLE_128B_BASE32B (TMA "128B_ATOM_32B").
 #include <cstdlib>
@@ -41,15 +43,16 @@ namespace lpy {
 namespace tf32 {
 
 constexpr int BM = 128, BN = 256, BK = 16;   // BM rows per CTA; BN columns per tile
-constexpr int THREADS = 320;                 // 10 warps
-constexpr int COMBO_THREADS = 256;           // warps 2-9: transform + promotion + epilogue
-constexpr int COMBO_WARPS = COMBO_THREADS / 32;
+constexpr int THREADS = 512;                 // 16 warps = 4 warpgroups
+constexpr int XFORM_WARP0 = 4, XFORM_WARPS = 4;
+constexpr int EPI_WARP0 = 8, EPI_WARPS = 8;
+constexpr int REGS_CTRL = 56, REGS_XFORM = 72, REGS_EPI = 192;   // 128*56 + 128*72 + 256*192 = 65536
 constexpr uint32_t TMEM_COLS = 512;          // 2 partial buffers x 256 columns
 
 template <int CG>
 struct Cfg {
     static constexpr int BN_CTA = BN / CG;                       // B columns staged per CTA
-    static constexpr int STAGES = CG == 2 ? 6 : 4;
+    static constexpr int STAGES = CG == 2 ? 7 : 4;
     static constexpr uint32_t A_BYTES = BM * BK * 4;             // 8 KB
     static constexpr uint32_t B_BYTES = BN_CTA * BK * 4;         // 16 KB / CG
     static constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;     // TMA transaction per stage
@@ -63,7 +66,20 @@ struct Params {
     int64_t ldc;
     int tiles_m, tiles_n, num_tiles, k_blocks, group, promote;
     int c_vec;
+    long long *trace;   // diagnostics build only (-DLPY_TRACE): per-CTA cycle counters
 };
+
+// Cycle accounting for the diagnostics build (liblpy_trace.so); compiled out of
+// the product library.  Slots per CTA: 0 MMA total, 1 MMA wait(ready), 2 MMA
+// wait(acce), 3 producer wait(empty), 4 transform wait(full), 5 epilogue
+// wait(accf), 6 transform busy, 7 epilogue busy.
+#ifdef LPY_TRACE
+#define TR_T0(v) const long long v = clock64()
+#define TR_ADD(slot, v) (tr[slot] += clock64() - (v))
+#else
+#define TR_T0(v) (void)0
+#define TR_ADD(slot, v) (void)0
+#endif
 
 __device__ __forceinline__ void tile_coords(int t, const Params &p, int &tm, int &tn) {
     const int per_group = p.group * p.tiles_n;
@@ -129,12 +145,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&ready[s], CG * COMBO_WARPS);
+            mbar_init(&ready[s], CG * XFORM_WARPS);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&accf[b], 1);
-            mbar_init(&acce[b], CG * COMBO_WARPS);
+            mbar_init(&acce[b], CG * EPI_WARPS);
         }
         fence_mbar_init();
     }
@@ -146,174 +162,196 @@ __global__ void __launch_bounds__(THREADS, 1)
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const int parts_per_tile = (p.k_blocks + p.promote - 1) / p.promote;
+#ifdef LPY_TRACE
+    long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
 
-    if (warp == 0) {
-        // ------------------------------------------------ TMA producer
-        if (lane == 0) {
-            tma_prefetch_desc(&tmA);
-            tma_prefetch_desc(&tmB);
-            int s = 0;
-            uint32_t ph = 0;
-            for (int t = unit0; t < p.num_tiles; t += units) {
-                int tm, tn;
-                tile_coords(t, p, tm, tn);
-                const int m0 = tm * (BM * CG) + rank * BM;
-                const int n0 = tn * BN + rank * C_::BN_CTA;
-                for (int kb = 0; kb < p.k_blocks; ++kb) {
-                    mbar_wait(&empty[s], ph ^ 1);
-                    uint8_t *sa = stages + s * STAGE_BYTES;
-                    uint8_t *sb = sa + A_BYTES;
-                    mbar_arrive_expect_tx(&full[s], RAW_BYTES);
-                    const int k0 = kb * BK;
-                    if constexpr (AMN) {
+    if (warp < XFORM_WARP0) {
+        setmaxnreg_dec<REGS_CTRL>();
+        if (warp == 0) {
+            // ------------------------------------------------ TMA producer
+            if (lane == 0) {
+                tma_prefetch_desc(&tmA);
+                tma_prefetch_desc(&tmB);
+                int s = 0;
+                uint32_t ph = 0;
+                for (int t = unit0; t < p.num_tiles; t += units) {
+                    int tm, tn;
+                    tile_coords(t, p, tm, tn);
+                    const int m0 = tm * (BM * CG) + rank * BM;
+                    const int n0 = tn * BN + rank * C_::BN_CTA;
+                    for (int kb = 0; kb < p.k_blocks; ++kb) {
+                        TR_T0(t_w);
+                        mbar_wait(&empty[s], ph ^ 1);
+                        TR_ADD(3, t_w);
+                        uint8_t *sa = stages + s * STAGE_BYTES;
+                        uint8_t *sb = sa + A_BYTES;
+                        mbar_arrive_expect_tx(&full[s], RAW_BYTES);
+                        const int k0 = kb * BK;
+                        if constexpr (AMN) {
 #pragma unroll
-                        for (int j = 0; j < BM / 32; ++j) tma_load_2d(sa + j * 2048, &tmA, &full[s], m0 + 32 * j, k0);
-                    } else {
-                        tma_load_2d(sa, &tmA, &full[s], k0, m0);
-                    }
-                    if constexpr (BMN) {
+                            for (int j = 0; j < BM / 32; ++j)
+                                tma_load_2d(sa + j * 2048, &tmA, &full[s], m0 + 32 * j, k0);
+                        } else {
+                            tma_load_2d(sa, &tmA, &full[s], k0, m0);
+                        }
+                        if constexpr (BMN) {
 #pragma unroll
-                        for (int j = 0; j < C_::BN_CTA / 32; ++j)
-                            tma_load_2d(sb + j * 2048, &tmB, &full[s], n0 + 32 * j, k0);
-                    } else {
-                        tma_load_2d(sb, &tmB, &full[s], k0, n0);
+                            for (int j = 0; j < C_::BN_CTA / 32; ++j)
+                                tma_load_2d(sb + j * 2048, &tmB, &full[s], n0 + 32 * j, k0);
+                        } else {
+                            tma_load_2d(sb, &tmB, &full[s], k0, n0);
+                        }
+                        if (++s == STAGES) { s = 0; ph ^= 1; }
                     }
-                    if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
             }
-        }
-    } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer (leader CTA)
-        if (lane == 0 && rank == 0) {
+        } else if (warp == 1 && rank == 0) {
+            // ------------------------------------------------ MMA issuer (leader CTA)
+            // The whole warp runs the loop (converged, so descriptors stay in
+            // uniform registers) and one elected lane issues: an issue path that
+            // rebuilt descriptors per MMA through R2UR waterfalls could not keep
+            // up with 128-cycle MMAs.
             constexpr uint32_t idesc = umma_idesc_tf32(BM * CG, BN, AMN ? 1 : 0, BMN ? 1 : 0);
+            // stage s adds s * STAGE_BYTES >> 4 to the descriptors' start-address field
+            const uint32_t sa0 = smem_u32(stages), sb0 = sa0 + A_BYTES;
+            const uint64_t dab[2] = {op_desc<AMN>(sa0, 0), op_desc<AMN>(sa0, 1)};
+            const uint64_t dbb[2] = {op_desc<BMN>(sb0, 0), op_desc<BMN>(sb0, 1)};
+            constexpr uint64_t SMALL = RAW_BYTES >> 4, STEP = STAGE_BYTES >> 4;
             int s = 0;
             uint32_t ph = 0;
             uint32_t npart = 0;   // partials issued by this pair
+            TR_T0(t_all);
             for (int t = unit0; t < p.num_tiles; t += units) {
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     const bool first = (kb % p.promote) == 0;
+                    const bool last = (kb % p.promote) == p.promote - 1 || kb == p.k_blocks - 1;
                     const uint32_t b = npart & 1;
                     if (first) {
-                        mbar_wait_cluster(&acce[b], ((npart >> 1) & 1) ^ 1);   // buffer drained (both CTAs)
+                        TR_T0(t_e);
+                        mbar_wait(&acce[b], ((npart >> 1) & 1) ^ 1);   // buffer drained (both CTAs)
+                        TR_ADD(2, t_e);
                         tc_fence_after();
                     }
-                    mbar_wait_cluster(&ready[s], ph);
+                    TR_T0(t_r);
+                    mbar_wait(&ready[s], ph);
+                    TR_ADD(1, t_r);
                     tc_fence_after();
-                    const uint32_t sa = smem_u32(stages + s * STAGE_BYTES);
-                    const uint32_t sb = sa + A_BYTES;
                     const uint32_t d = tmem + b * 256;
+                    const uint64_t off = uint64_t(s) * STEP;
+                    if (elect_one()) {
 #pragma unroll
-                    for (int sub = 0; sub < BK / 8; ++sub) {
-                        const uint64_t a_big = op_desc<AMN>(sa, sub), b_big = op_desc<BMN>(sb, sub);
-                        const uint64_t a_small = op_desc<AMN>(sa + RAW_BYTES, sub);
-                        const uint64_t b_small = op_desc<BMN>(sb + RAW_BYTES, sub);
-                        umma_tf32_cg<CG>(d, a_big, b_small, idesc, (first && sub == 0) ? 0u : 1u);
-                        umma_tf32_cg<CG>(d, a_small, b_big, idesc, 1u);
-                        umma_tf32_cg<CG>(d, a_big, b_big, idesc, 1u);
-                    }
-                    umma_commit_cg<CG>(&empty[s]);
-                    if (++s == STAGES) { s = 0; ph ^= 1; }
-                    if ((kb % p.promote) == p.promote - 1 || kb == p.k_blocks - 1) {
-                        umma_commit_cg<CG>(&accf[b]);
-                        ++npart;
-                    }
-                }
-            }
-        }
-    } else {
-        // ------------------------------------------------ split transform + promotion + epilogue
-        // Warps 2-9 transform every stage (raw -> small) and, whenever a TMEM
-        // partial is complete, fold it into their fp32 register accumulators
-        // (checked without blocking after each stage; the MMA only needs a
-        // buffer back `promote` stages later).  After a tile's last partial
-        // they store this CTA's 128 x 256 block of C.
-        const int ctid = threadIdx.x - 64;       // 0..255
-        const int quad = warp & 3;               // TMEM lanes 32*quad .. +31 (hardware rule)
-        const int half = (warp - 2) >> 2;        // columns 128*half .. +127
-        const uint32_t lane_base = uint32_t(quad * 32) << 16;
-        float acc[128];
-#pragma unroll
-        for (int j = 0; j < 128; ++j) acc[j] = 0.f;
-        int t_prom = unit0, part = 0;            // next partial to promote: (tile, part)
-        uint32_t np = 0;                         // partials promoted so far
-
-        auto promote_ready = [&](bool block) {
-            while (t_prom < p.num_tiles) {
-                const uint32_t b = np & 1, par = (np >> 1) & 1;
-                if (block) {
-                    mbar_wait(&accf[b], par);
-                } else {
-                    uint32_t ok = lane == 0 ? mbar_test(&accf[b], par) : 0u;
-                    if (!__shfl_sync(0xffffffffu, ok, 0)) return;
-                }
-                tc_fence_after();
-                const uint32_t base = tmem + lane_base + b * 256 + half * 128;
-#pragma unroll
-                for (int c = 0; c < 128; c += 16) {
-                    uint32_t v0[16];
-                    tmem_ld_x16(base + c, v0);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) acc[c + j] += __uint_as_float(v0[j]);
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) arrive_leader<CG>(&acce[b]);
-                ++np;
-                if (++part == parts_per_tile) {
-                    int tm, tn;
-                    tile_coords(t_prom, p, tm, tn);
-                    const int row = tm * (BM * CG) + rank * BM + quad * 32 + lane;
-                    if (row < p.M) {
-                        float *crow = p.C + int64_t(row) * p.ldc;
-                        const int col0 = tn * BN + half * 128;
-#pragma unroll
-                        for (int j = 0; j < 128; j += 4) {
-                            const int col = col0 + j;
-                            if (p.c_vec && col + 3 < p.N) {
-                                *reinterpret_cast<float4 *>(crow + col) =
-                                    make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-                            } else {
-#pragma unroll
-                                for (int e = 0; e < 4; ++e)
-                                    if (col + e < p.N) crow[col + e] = acc[j + e];
-                            }
+                        for (int sub = 0; sub < BK / 8; ++sub) {
+                            const uint64_t a_big = dab[sub] + off, b_big = dbb[sub] + off;
+                            umma_tf32_cg<CG>(d, a_big, b_big + SMALL, idesc, (first && sub == 0) ? 0u : 1u);
+                            umma_tf32_cg<CG>(d, a_big + SMALL, b_big, idesc, 1u);
+                            umma_tf32_cg<CG>(d, a_big, b_big, idesc, 1u);
                         }
+                        umma_commit_cg<CG>(&empty[s]);
+                        if (last) umma_commit_cg<CG>(&accf[b]);
                     }
-#pragma unroll
-                    for (int j = 0; j < 128; ++j) acc[j] = 0.f;
-                    part = 0;
-                    t_prom += units;
+                    __syncwarp();
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                    if (last) ++npart;
                 }
             }
-        };
-
+            TR_ADD(0, t_all);
+        }
+    } else if (warp < EPI_WARP0) {
+        // ------------------------------------------------ split transform (WG1)
+        setmaxnreg_dec<REGS_XFORM>();
+        const int xt = threadIdx.x - XFORM_WARP0 * 32;   // 0..127
+        constexpr int PER_THREAD = int(RAW_BYTES / 16) / (XFORM_WARPS * 32);
         int s = 0;
         uint32_t ph = 0;
         for (int t = unit0; t < p.num_tiles; t += units) {
             for (int kb = 0; kb < p.k_blocks; ++kb) {
+                TR_T0(t_f);
                 mbar_wait(&full[s], ph);
+                TR_ADD(4, t_f);
+                TR_T0(t_x);
                 const float4 *src = reinterpret_cast<const float4 *>(stages + s * STAGE_BYTES);
                 float4 *dst = reinterpret_cast<float4 *>(stages + s * STAGE_BYTES + RAW_BYTES);
-#pragma unroll 3
-                for (int i = 0; i < int(RAW_BYTES / 16) / COMBO_THREADS; ++i) {
-                    float4 v = src[ctid + i * COMBO_THREADS];
+#pragma unroll 4
+                for (int i = 0; i < PER_THREAD; ++i) {
+                    float4 v = src[xt + i * XFORM_WARPS * 32];
                     v.x = tf32_small(v.x);
                     v.y = tf32_small(v.y);
                     v.z = tf32_small(v.z);
                     v.w = tf32_small(v.w);
-                    dst[ctid + i * COMBO_THREADS] = v;
+                    dst[xt + i * XFORM_WARPS * 32] = v;
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) arrive_leader<CG>(&ready[s]);
                 if (++s == STAGES) { s = 0; ph ^= 1; }
-                promote_ready(false);
+                TR_ADD(6, t_x);
             }
         }
-        promote_ready(true);
+    } else {
+        // ------------------------------------------------ promotion + epilogue (WG2, WG3)
+        setmaxnreg_inc<REGS_EPI>();
+        const int quad = warp & 3;                       // TMEM lanes 32*quad .. +31 (hardware rule)
+        const int half = (warp - EPI_WARP0) >> 2;        // columns 128*half .. +127
+        const uint32_t lane_base = uint32_t(quad * 32) << 16;
+        const int parts_per_tile = (p.k_blocks + p.promote - 1) / p.promote;
+        uint32_t np = 0;                                 // partials promoted so far
+        for (int t = unit0; t < p.num_tiles; t += units) {
+            float acc[128];
+#pragma unroll
+            for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+            for (int part = 0; part < parts_per_tile; ++part, ++np) {
+                const uint32_t b = np & 1;
+                TR_T0(t_w);
+                mbar_wait(&accf[b], (np >> 1) & 1);
+                TR_ADD(5, t_w);
+                TR_T0(t_b);
+                tc_fence_after();
+                const uint32_t base = tmem + lane_base + b * 256 + half * 128;
+#pragma unroll
+                for (int c = 0; c < 128; c += 32) {
+                    uint32_t v0[16], v1[16];
+                    tmem_ld_x16(base + c, v0);
+                    tmem_ld_x16(base + c + 16, v1);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        acc[c + j] += __uint_as_float(v0[j]);
+                        acc[c + 16 + j] += __uint_as_float(v1[j]);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) arrive_leader<CG>(&acce[b]);
+                TR_ADD(7, t_b);
+            }
+            int tm, tn;
+            tile_coords(t, p, tm, tn);
+            const int row = tm * (BM * CG) + rank * BM + quad * 32 + lane;
+            if (row < p.M) {
+                float *crow = p.C + int64_t(row) * p.ldc;
+                const int col0 = tn * BN + half * 128;
+#pragma unroll
+                for (int j = 0; j < 128; j += 4) {
+                    const int col = col0 + j;
+                    if (p.c_vec && col + 3 < p.N) {
+                        *reinterpret_cast<float4 *>(crow + col) =
+                            make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (col + e < p.N) crow[col + e] = acc[j + e];
+                    }
+                }
+            }
+        }
     }
+#ifdef LPY_TRACE
+    if (p.trace && lane == 0 && (warp <= 1 || warp == XFORM_WARP0 || warp == EPI_WARP0))
+        for (int i = 0; i < 8; ++i)
+            if (tr[i]) atomicAdd(reinterpret_cast<unsigned long long *>(&p.trace[blockIdx.x * 8 + i]),
+                                 (unsigned long long)tr[i]);
+#endif
 
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
@@ -346,6 +384,8 @@ static cudaError_t launch_t(const CUtensorMap &ta, const CUtensorMap &tb, const 
     return cudaLaunchKernelEx(&cfg, kern, ta, tb, prm);
 }
 
+static long long *g_trace = nullptr;   // set by lpy_trace_set_buffer (diagnostics build)
+
 template <int CG>
 static cudaError_t launch_cg(const Problem &p, const Knobs &kn, cudaStream_t s) {
     const bool AMN = (p.la == 1);   // column-major A: M contiguous
@@ -370,6 +410,7 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, cudaStream_t s) 
     prm.group = kn.raster_group > 0 ? kn.raster_group : 16 / CG;
     prm.promote = kn.promote_kblocks > 0 ? kn.promote_kblocks : 8;   // 128 of K per TMEM partial
     prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
+    prm.trace = g_trace;
     int units = (kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms) / CG;  // CTAs (pairs) in the grid
     if (units > prm.num_tiles) units = prm.num_tiles;
     if (units < 1) units = 1;
@@ -396,3 +437,9 @@ cudaError_t launch_3xtf32(const Problem &p, const Knobs &kn, cudaStream_t s) {
 }
 
 }  // namespace lpy
+
+#ifdef LPY_TRACE
+// Diagnostics build only: device buffer of 8 counters per CTA, accumulated by
+// every subsequent 3xTF32 launch (zero it between runs).
+extern "C" void lpy_trace_set_buffer(long long *dev) { lpy::tf32::g_trace = dev; }
+#endif

@@ -215,3 +215,87 @@ int lpy_probe_ffma_rate(float *out, int iters, int blocks, int threads, int pair
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- MMA rate per operand format
+// Back-to-back kind::tf32 MMAs over a 32-wide k panel in the given operand
+// formats (see `offset`), single CTA (M=128) or CTA pair (M=256, cluster of 2).
+namespace lpy {
+namespace probe {
+template <int CG>
+__global__ void umma_rate_fmt_kernel(int N, int fa, int fb, int iters, long long *cycles) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t *base = smem_raw + (((raw + 1023) & ~1023u) - raw);
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int nb = N / CG;   // B rows staged per CTA
+    for (int i = threadIdx.x; i < (128 + nb) * 32; i += blockDim.x)
+        reinterpret_cast<float *>(base)[i] = 1.0f;
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    if (threadIdx.x < 32) {
+        tmem_alloc_cg<CG>(&tmem_base, 256);
+        tmem_relinquish_cg<CG>();
+    }
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    if (threadIdx.x == 0 && rank == 0) {
+        const uint32_t idesc = umma_idesc_tf32(128 * CG, N, fa & 1, fb & 1);
+        const uint32_t sa = smem_u32(base), sb = smem_u32(base) + 128 * 128;
+        // descriptors of the 4 k-slices, computed once (the loop must not be issue-bound)
+        const uint64_t a0 = desc(fa, sa, 0, 128), a1 = desc(fa, sa, 1, 128), a2 = desc(fa, sa, 2, 128),
+                       a3 = desc(fa, sa, 3, 128);
+        const uint64_t b0 = desc(fb, sb, 0, nb), b1 = desc(fb, sb, 1, nb), b2 = desc(fb, sb, 2, nb),
+                       b3 = desc(fb, sb, 3, nb);
+        const bool same = iters < 0;          // negative iters: repeat slice 0 (operand reuse)
+        if (same) iters = -iters;
+        long long t0 = clock64();
+        for (int i = 0; i < iters; i += 4) {
+            umma_tf32_cg<CG>(tmem_base, a0, b0, idesc, i > 0 ? 1u : 0u);
+            umma_tf32_cg<CG>(tmem_base, same ? a0 : a1, same ? b0 : b1, idesc, 1u);
+            umma_tf32_cg<CG>(tmem_base, same ? a0 : a2, same ? b0 : b2, idesc, 1u);
+            umma_tf32_cg<CG>(tmem_base, same ? a0 : a3, same ? b0 : b3, idesc, 1u);
+        }
+        umma_commit_cg<CG>(&bar);
+        mbar_wait(&bar, 0);
+        long long t1 = clock64();
+        if (blockIdx.x == 0) *cycles = t1 - t0;
+    } else if (threadIdx.x == 0) {
+        mbar_wait(&bar, 0);
+    }
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    if (threadIdx.x < 32) tmem_dealloc_cg<CG>(tmem_base, 256);
+}
+}  // namespace probe
+}  // namespace lpy
+
+extern "C" int lpy_probe_umma_rate_fmt(int N, int fa, int fb, int iters, int ctas, int cg,
+                                       long long *cycles_dev, void *stream) {
+    const size_t smem = 1024 + size_t(128 + 256) * 32 * 4;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cg;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cg == 2) {
+        cudaFuncSetAttribute(lpy::probe::umma_rate_fmt_kernel<2>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        return int(cudaLaunchKernelEx(&cfg, lpy::probe::umma_rate_fmt_kernel<2>, N, fa, fb, iters, cycles_dev));
+    }
+    cudaFuncSetAttribute(lpy::probe::umma_rate_fmt_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    return int(cudaLaunchKernelEx(&cfg, lpy::probe::umma_rate_fmt_kernel<1>, N, fa, fb, iters, cycles_dev));
+}

@@ -146,3 +146,22 @@ def test_ffma_rate(probe):
         flops = 2.0 * 16 * iters * blocks * threads
         RESULTS[f"ffma_tflops_pair{pair}"] = flops / ms / 1e9
     print(RESULTS)
+
+
+def test_mma_rate_per_operand_format(probe):
+    """Cycles per kind::tf32 MMA (N=256, K=8) for each smem operand format, single
+    CTA (M=128) and CTA pair (M=256).  Full rate is 128 cycles."""
+    probe.lpy_probe_umma_rate_fmt.argtypes = [ctypes.c_int] * 6 + [ctypes.c_void_p, ctypes.c_void_p]
+    cyc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    iters = 4000
+    for cg in (1, 2):
+        for fa in range(4):
+            for fb in range(4):
+                for same in (False, True):
+                    rc = probe.lpy_probe_umma_rate_fmt(256, fa, fb, -iters if same else iters, 148, cg,
+                                                       cyc.data_ptr(), None)
+                    torch.cuda.synchronize()
+                    assert rc == 0
+                    key = f"cycles_per_mma_cg{cg}_fa{fa}_fb{fb}" + ("_same" if same else "")
+                    RESULTS[key] = cyc.item() / iters
+    print({k: v for k, v in RESULTS.items() if k.startswith("cycles_per_mma_cg")})
