@@ -93,7 +93,7 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device_index: int, period_ms: int = 50):
+    def __init__(self, device_index: int, period_ms: int = 20):
         import shutil
         import tempfile
         self.period = period_ms
@@ -352,7 +352,7 @@ def time_e2e(args, path, rank, world, device):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--n", type=int, default=8192)
     ap.add_argument("--path", default="auto", choices=["auto", "ffma", "3xtf32"])

@@ -50,6 +50,25 @@ struct Params {
     int c_vec;  // C base and ldc allow 16-byte stores
 };
 
+// Packed fp32 pairs for FFMA2.  c += a * b with c, b packed (lo, hi) pairs and
+// the scalar a broadcast: fma.rn.f32x2 = two fp32 RN fused multiply-adds,
+// bit-identical to two FFMAs, in half the issue slots.
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void unpack2(unsigned long long v, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ void ffma2(unsigned long long &c, float a, unsigned long long b) {
+    asm("{\n\t.reg .b64 x;\n\t"
+        "mov.b64 x, {%1, %1};\n\t"
+        "fma.rn.f32x2 %0, x, %2, %0;\n\t}"
+        : "+l"(c)
+        : "f"(a), "l"(b));
+}
+
 __device__ __forceinline__ void tile_coords(int t, const Params &p, int &tm, int &tn) {
     const int per_group = p.group * p.tiles_n;
     const int g = t / per_group;
@@ -173,11 +192,23 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         int tm, tn;
         tile_coords(t, p, tm, tn);
-        float acc[8][8];
+        // Accumulators as packed pairs for FFMA2, paired along the operand whose
+        // fragment arrives with adjacent elements from one LDS.128:
+        //   PAIR_J (B MN-major): acc2[i][jp] = (acc(i, 2jp), acc(i, 2jp+1)), a broadcast
+        //   PAIR_I (A MN-major, B K-major): acc2[ip][j] = (acc(2ip, j), acc(2ip+1, j)), b broadcast
+        // Both K-major: plain FFMA (pairing would cost a register move per FFMA2).
+        constexpr bool PAIR_J = !BKM, PAIR_I = BKM && !AK;
+        constexpr int P0 = PAIR_I ? 4 : 8, P1 = PAIR_I ? 8 : 4;
+        unsigned long long acc2[P0][P1];
+        float accf[8][8];
+#pragma unroll
+        for (int i = 0; i < P0; ++i)
+#pragma unroll
+            for (int j = 0; j < P1; ++j) acc2[i][j] = 0ull;
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+            for (int j = 0; j < 8; ++j) accf[i][j] = 0.f;
 
         for (int kb = 0; kb < p.k_blocks; ++kb) {
             mbar_wait(&full[stage], phase);
@@ -189,11 +220,30 @@ __global__ void __launch_bounds__(THREADS, 1)
                 load_a<AK>(sa, kq, wm, lm, a);
                 load_b<BKM>(sb, kq, wn, ln, b);
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
+                for (int k = 0; k < 4; ++k) {
+                    if constexpr (PAIR_J) {
+                        unsigned long long bp[4];   // adjacent registers: packing is free
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                        for (int jp = 0; jp < 4; ++jp) bp[jp] = pack2(b[k][2 * jp], b[k][2 * jp + 1]);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[k][i], b[k][j], acc[i][j]);
+                        for (int i = 0; i < 8; ++i)
+#pragma unroll
+                            for (int jp = 0; jp < 4; ++jp) ffma2(acc2[i][jp], a[k][i], bp[jp]);
+                    } else if constexpr (PAIR_I) {
+                        unsigned long long ap[4];
+#pragma unroll
+                        for (int ip = 0; ip < 4; ++ip) ap[ip] = pack2(a[k][2 * ip], a[k][2 * ip + 1]);
+#pragma unroll
+                        for (int ip = 0; ip < 4; ++ip)
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) ffma2(acc2[ip][j], b[k][j], ap[ip]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) accf[i][j] = fmaf(a[k][i], b[k][j], accf[i][j]);
+                    }
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
@@ -201,6 +251,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
 
         // ------------------------------------------------ epilogue (ragged-edge stores)
+        float acc[8][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if constexpr (PAIR_J) {
+                    if (j % 2 == 0) unpack2(acc2[i][j / 2], acc[i][j], acc[i][j + 1]);
+                } else if constexpr (PAIR_I) {
+                    if (i % 2 == 0) unpack2(acc2[i / 2][j], acc[i][j], acc[i + 1][j]);
+                } else {
+                    acc[i][j] = accf[i][j];
+                }
+            }
         const int m0 = tm * BM, n0 = tn * BN;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
