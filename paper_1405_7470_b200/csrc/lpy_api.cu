@@ -1,6 +1,7 @@
 // C-ABI front end (include/lpy.h): validation, layout canonicalisation,
 // degenerate sizes, aligned repack, path selection, launch, and the host-buffer
 // end-to-end entry point.  No torch types anywhere; plain pointers and sizes.
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -95,6 +96,15 @@ lpy_status device_info(DeviceInfo &out) {
             return cuda_fail(e);
         d.ok = true;
         cache[dev] = d;
+        // Keep freed stream-ordered scratch in the device's default pool instead of
+        // returning it to the driver at every synchronisation: the end-to-end entry
+        // point allocates and frees ~800 MB per call at n = 8192, and re-mapping it
+        // each time cost more than the copies themselves.
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
     }
     out = cache[dev];
     // The kernels are built for sm_100a only (tcgen05 / TMA); anything else would
@@ -279,8 +289,8 @@ lpy_status lpy_gemm_f32_host(int64_t M, int64_t N, int64_t K, const float *A, in
     if ((st = device_info(dev)) != LPY_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
 
-    // Device copies with 16-byte-aligned leading dimensions: the H2D copy does
-    // the repack for free.
+    // Device copies with 16-byte-aligned leading dimensions (the H2D copy does
+    // the repack for free), allocated stream-ordered on the caller's stream.
     Operand *ops[3] = {&oa, &ob, &oc};
     float *dev_buf[3] = {nullptr, nullptr, nullptr};
     int64_t dev_ld[3] = {1, 1, 1};
@@ -290,19 +300,86 @@ lpy_status lpy_gemm_f32_host(int64_t M, int64_t N, int64_t K, const float *A, in
         dev_ld[i] = o.inner() > 0 ? (o.inner() + 3) & ~int64_t(3) : 4;
         if (o.extent() == 0) continue;
         e = cudaMallocAsync(reinterpret_cast<void **>(&dev_buf[i]), size_t(o.lines() * dev_ld[i]) * 4, s);
-        if (e == cudaSuccess && i < 2)
-            e = copy_lines(dev_buf[i], dev_ld[i], o.p, o.ld, o.inner(), o.lines(), cudaMemcpyHostToDevice, s);
     }
-    if (e == cudaSuccess) {
-        st = lpy_gemm_f32_ex(M, N, K, dev_buf[0], dev_ld[0], layout_a, dev_buf[1], dev_ld[1], layout_b,
-                             dev_buf[2], dev_ld[2], layout_c, stream, path, nullptr);
-        if (st == LPY_OK)
-            e = copy_lines(C, ldc, dev_buf[2], dev_ld[2], oc.inner(), oc.lines(), cudaMemcpyDeviceToHost, s);
+
+    // Row-panel pipeline over three internal streams: H2D of B then of each A
+    // panel, the panel products as their inputs land, and D2H of each C panel
+    // as soon as it is computed -- so the C download and the products hide
+    // under the A upload (PCIe is full duplex).  Panels are multiples of 128
+    // rows (the output tile), at most 8 of them.
+    const int64_t prow = M <= 1024 ? M : ((M + 7) / 8 + 127) / 128 * 128;
+    const int npanel = int((M + prow - 1) / prow);
+    cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_b = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_a[8] = {}, ev_c[8] = {};
+    auto mk_stream = [&](cudaStream_t *x) {
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(x, cudaStreamNonBlocking);
+    };
+    auto mk_event = [&](cudaEvent_t *x) {
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(x, cudaEventDisableTiming);
+    };
+    mk_stream(&sh); mk_stream(&sc); mk_stream(&sd);
+    mk_event(&ev_fork); mk_event(&ev_b); mk_event(&ev_done);
+    for (int q = 0; q < npanel; ++q) { mk_event(&ev_a[q]); mk_event(&ev_c[q]); }
+
+    // Copy rows [r0, r1) of an M-row operand (A or C) between host and device.
+    auto copy_rows = [&](int i, int64_t r0, int64_t r1, cudaMemcpyKind kind, cudaStream_t st_) {
+        const Operand &o = *ops[i];
+        float *host = const_cast<float *>(o.p);
+        const bool row = o.layout == LPY_ROW_MAJOR;
+        const int64_t cols = i == 0 ? K : N;
+        if (cols == 0 || r1 <= r0) return cudaSuccess;
+        float *h = host + (row ? r0 * o.ld : r0);
+        float *d = dev_buf[i] + (row ? r0 * dev_ld[i] : r0);
+        const int64_t inner = row ? cols : r1 - r0, lines = row ? r1 - r0 : cols;
+        return kind == cudaMemcpyHostToDevice
+                   ? copy_lines(d, dev_ld[i], h, o.ld, inner, lines, kind, st_)
+                   : copy_lines(h, o.ld, d, dev_ld[i], inner, lines, kind, st_);
+    };
+
+    if (e == cudaSuccess) e = cudaEventRecord(ev_fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sh, ev_fork, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, ev_fork, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, ev_fork, 0);
+    if (e == cudaSuccess && ob.extent() > 0)
+        e = copy_lines(dev_buf[1], dev_ld[1], ob.p, ob.ld, ob.inner(), ob.lines(), cudaMemcpyHostToDevice, sh);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_b, sh);
+    for (int q = 0; q < npanel && e == cudaSuccess; ++q) {
+        const int64_t r0 = q * prow, r1 = std::min(M, r0 + prow);
+        e = copy_rows(0, r0, r1, cudaMemcpyHostToDevice, sh);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_a[q], sh);
+    }
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, ev_b, 0);
+    for (int q = 0; q < npanel && e == cudaSuccess && st == LPY_OK; ++q) {
+        const int64_t r0 = q * prow, r1 = std::min(M, r0 + prow);
+        e = cudaStreamWaitEvent(sc, ev_a[q], 0);
+        if (e != cudaSuccess) break;
+        const bool arow = layout_a == LPY_ROW_MAJOR, crow = layout_c == LPY_ROW_MAJOR;
+        const float *ap = dev_buf[0] ? dev_buf[0] + (arow ? r0 * dev_ld[0] : r0) : nullptr;
+        float *cp = dev_buf[2] + (crow ? r0 * dev_ld[2] : r0);
+        st = lpy_gemm_f32_ex(r1 - r0, N, K, ap, dev_ld[0], layout_a, dev_buf[1], dev_ld[1], layout_b, cp,
+                             dev_ld[2], layout_c, sc, path, nullptr);
+        if (st == LPY_OK) e = cudaEventRecord(ev_c[q], sc);
+        if (e == cudaSuccess && st == LPY_OK) e = cudaStreamWaitEvent(sd, ev_c[q], 0);
+        if (e == cudaSuccess && st == LPY_OK) e = copy_rows(2, r0, r1, cudaMemcpyDeviceToHost, sd);
+    }
+    // join everything back onto the caller's stream, then free and synchronise
+    cudaStream_t side[3] = {sh, sc, sd};
+    for (cudaStream_t x : side) {
+        if (x && ev_done && cudaEventRecord(ev_done, x) == cudaSuccess) cudaStreamWaitEvent(s, ev_done, 0);
     }
     for (int i = 0; i < 3; ++i)
         if (dev_buf[i]) cudaFreeAsync(dev_buf[i], s);
     cudaError_t e2 = cudaStreamSynchronize(s);
     if (e == cudaSuccess) e = e2;
+    for (cudaStream_t x : side)
+        if (x) cudaStreamDestroy(x);
+    for (cudaEvent_t x : {ev_fork, ev_b, ev_done})
+        if (x) cudaEventDestroy(x);
+    for (int q = 0; q < npanel; ++q) {
+        if (ev_a[q]) cudaEventDestroy(ev_a[q]);
+        if (ev_c[q]) cudaEventDestroy(ev_c[q]);
+    }
     if (st != LPY_OK) return st;
     return e == cudaSuccess ? LPY_OK : cuda_fail(e);
 }

@@ -173,6 +173,24 @@ def test_torch_binding_and_host_entry():
     assert np.isnan(cbuf.reshape(-1)[200:203]).all()      # host C padding untouched
 
 
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("la,lb,lc", [(0, 0, 0), (1, 1, 1), (0, 1, 1), (1, 0, 0)])
+def test_host_entry_pipelined_panels(path, la, lb, lc):
+    """lpy_gemm_f32_host splits M > 1024 into row panels whose H2D / product /
+    D2H overlap on internal streams; every layout and a padded host ld."""
+    M, N, K = 2500, 700, 300
+    A, B = inputs(M, N, K, seed=12)
+    abuf, lda = synth.store(A, la, synth.min_ld(M, K, la) + 3)
+    bbuf, ldb = synth.store(B, lb, synth.min_ld(K, N, lb) + 1)
+    cbuf, ldc = synth.store(np.zeros((M, N), np.float32), lc, synth.min_ld(M, N, lc) + 5,
+                            pad_value=np.nan)
+    lpy.gemm_host(M, N, K, abuf, lda, la, bbuf, ldb, lb, cbuf, ldc, lc, path=path)
+    C = synth.load_logical(cbuf, M, N, lc, ldc)
+    check(C, A, B)
+    lines, inner = (M, N) if lc == 0 else (N, M)
+    assert np.isnan(cbuf.reshape(-1)[inner:ldc]).all()        # host C padding untouched
+
+
 def test_errors_on_device():
     A = torch.zeros(4, 4, device="cuda")
     with pytest.raises(lpy.LpyError):
