@@ -242,21 +242,25 @@ def make_inputs(n, rank, world, chunks, device):
 def time_path(args, path, rank, world, device, dist_on):
     import torch
     import paper_1405_7470_b200 as lpy
-    from paper_1405_7470_b200.dist import rowpanel_gemm
+    from paper_1405_7470_b200.dist import choose_chunks, panel_bounds, rowpanel_gemm
     n = args.n
-    chunks = args.chunks if world > 1 else 1
+    r0_, r1_ = panel_bounds(n, world, rank)
+    chunks = (args.chunks or choose_chunks(r1_ - r0_, n,
+                                            torch.cuda.get_device_properties(device).multi_processor_count)
+              ) if dist_on else 1
     A, blocks, C, bounds, (r0, r1) = make_inputs(n, rank, world, chunks, device)
 
     def gemm_fn(a, b, c):
         lpy.gemm(a, b, out=c, path=path)
 
-    comm = torch.cuda.Stream() if world > 1 else None
+    comm = torch.cuda.Stream() if dist_on else None
+    cstreams = [torch.cuda.Stream(), torch.cuda.Stream()] if dist_on else None
 
     def step():
-        if world == 1:
+        if not dist_on:
             lpy.gemm(A, blocks[0], out=C, path=path)
         else:
-            rowpanel_gemm(A, blocks, C, bounds, gemm_fn=gemm_fn, comm_stream=comm)
+            rowpanel_gemm(A, blocks, C, bounds, gemm_fn=gemm_fn, comm_stream=comm, compute_streams=cstreams)
 
     for _ in range(args.warmup):
         step()
@@ -279,19 +283,46 @@ def time_path(args, path, rank, world, device, dist_on):
         torch.cuda.synchronize()
     total_ms = t0.elapsed_time(t1)
     kernel_ms = [a.elapsed_time(b) for a, b in per]
+    multi = None
     if dist_on:
         import torch.distributed as dist
-        t = torch.tensor([total_ms], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+
+        def max_ms(ms):
+            t = torch.tensor([ms], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+
+        def timed(fn, reps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            return max_ms(a.elapsed_time(b) / reps)
+
+        total_ms = max_ms(total_ms)
+        reps = max(3, min(args.steps, 10))
+        # the two halves of a step, each timed alone (max over ranks): B's broadcast
+        # (4*K*N bytes from rank 0) and this rank's panel products
+        bcast_ms = timed(lambda: [dist.broadcast(b, src=0) for b in blocks], reps)
+        gemm_ms = timed(lambda: rowpanel_gemm(A, blocks, C, bounds, gemm_fn=gemm_fn, comm_stream=comm,
+                                              compute_streams=cstreams, broadcast=False), reps)
+        nbytes = 4 * n * n
+        multi = {"total_ms": round(total_ms / args.steps, 4), "bcast_ms": round(bcast_ms, 4),
+                 "gemm_ms": round(gemm_ms, 4), "bcast_bytes": nbytes,
+                 "bcast_algbw_gbs": round(nbytes / (bcast_ms * 1e-3) / 1e9, 1), "chunks": len(bounds)}
         dist.barrier()
-        total_ms = float(t.item())
     # sampled parity of this run's output against the oracle (rank 0 panel)
     parity = None
     if rank == 0 and not args.no_parity:
         parity = sampled_parity(A, blocks, bounds, C, n, r0)
     _, chosen = lpy.lpy_select_path(r1 - r0, n, n, lpy.PATHS[path])
     return {"total_ms": total_ms, "kernel_ms": kernel_ms, "clocks": clk.summary(), "parity": parity,
-            "path": {1: "ffma", 2: "3xtf32"}[chosen], "launches_per_step": len(bounds)}
+            "path": {1: "ffma", 2: "3xtf32"}[chosen], "launches_per_step": len(bounds), "chunks": len(bounds),
+            "multi": multi}
 
 
 def sampled_parity(A, blocks, bounds, C, n, r0, count=512):
@@ -357,7 +388,10 @@ def main():
     ap.add_argument("--n", type=int, default=8192)
     ap.add_argument("--path", default="auto", choices=["auto", "ffma", "3xtf32"])
     ap.add_argument("--also", default="ffma", help="secondary path to report ('' for none)")
-    ap.add_argument("--chunks", type=int, default=4)
+    ap.add_argument("--chunks", type=int, default=0, help="B column blocks for N>1 (0 = ~1 wave each)")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the row-panel + NCCL broadcast step even at N=1 (exercises the N>1 path)")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
@@ -379,9 +413,14 @@ def main():
     lpy.load_library()
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    dist_on = world > 1
+    dist_on = world > 1 or args.force_dist
     if dist_on:
         import torch.distributed as dist
+        if "MASTER_ADDR" not in os.environ:          # --force-dist without torchrun
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=device)
 
     main_path = args.path
@@ -392,7 +431,7 @@ def main():
     also = None
     if args.also and args.also != main_path:
         also = time_path(args, args.also, rank, world, device, dist_on)
-    e2e = time_e2e(args, main_path, rank, world, device)
+    e2e = None if args.no_e2e else time_e2e(args, main_path, rank, world, device)
 
     if rank == 0:
         n = args.n
@@ -402,11 +441,11 @@ def main():
 
         def roof(r, path):
             bound, peak, note = roofline_peak(path)
-            kms = statistics.mean(r["kernel_ms"]) if world == 1 else None
-            if kms is None:        # multi-GPU: per-rank panel product time is not isolated
-                return {"bound": bound, "achieved": None, "peak": peak, "unit": "TFLOP/s",
-                        "frac": None, "traffic": None, "peak_note": note}
-            achieved = flops / (kms * 1e-3) / 1e12
+            if not dist_on:        # one GEMM launch per step: its CUDA-event time
+                kms, kflops = statistics.mean(r["kernel_ms"]), flops
+            else:                  # rank 0's panel products without the broadcast
+                kms, kflops = r["multi"]["gemm_ms"], flops / world
+            achieved = kflops / (kms * 1e-3) / 1e12
             traffic, tsrc = profile_traffic(path, n)
             return {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3),
                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -425,15 +464,18 @@ def main():
             "data": "synthetic: seeded SplitMix64 uniform[-1,1) fp32 on a 2^-23 grid",
             "config": {"workload": f"n={n} square fp32 C=A*B, row-major A/B/C (BASELINE config 4)",
                        "path": res["path"], "M": n, "N": n, "K": n,
-                       "parallelism": f"rowpanel{world}" + (f"+bcast_chunks{args.chunks}" if world > 1 else ""),
+                       "parallelism": f"rowpanel{world}" + (f"+nccl_bcast_B_chunks{res['chunks']}" if dist_on else ""),
                        "l2": "inputs larger than L2 (A, B, C 268 MB each > 126 MB), no flush"},
             "roofline": roof(res, res["path"]),
             "cpu_baseline": cpu,
-            "e2e": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in e2e.items()},
+            "e2e": ({k: (round(v, 3) if isinstance(v, float) else v) for k, v in e2e.items()}
+                    if e2e else None),
             "gpu_launches": res["launches_per_step"] * args.steps,
             "clocks": res["clocks"],
             "parity_sampled_max_norm_err": res["parity"],
         }
+        if dist_on:
+            line["multi_gpu"] = res["multi"]
         if also is not None:
             ams = also["total_ms"] / args.steps
             line["alt_path"] = {"path": also["path"], "value": round(flops / (ams * 1e-3) / 1e9, 1),

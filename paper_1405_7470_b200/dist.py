@@ -9,10 +9,13 @@ C[rows_r, :] = A[rows_r, :] B, so the only exchange is ONE broadcast of B
 To overlap the broadcast with the product, B is held in column-blocked
 storage: `chunks` contiguous blocks, block c a row-major K x w_c matrix
 (the same logical B, different storage -- the paper's layout tags).
-Block c is broadcast on a dedicated communication stream while the compute
-stream multiplies the already-arrived blocks: C[:, cols_c] = A_panel B_c is an
-lpy_gemm_f32 call writing a disjoint column block of C (ldc = N).  Chunk
-widths are multiples of 128 (the output tile) so each block is 16-byte aligned.
+Block c is broadcast on a dedicated communication stream; as soon as it has
+arrived, C[:, cols_c] = A_panel B_c (an lpy_gemm_f32 call writing a disjoint
+column block of C, ldc = N) runs on one of `compute_streams` streams, so the
+product of a block overlaps the broadcast of the next and, when one block's
+product does not fill the GPU, two blocks' products share it.  Chunk widths are
+multiples of 256 (the 3xTF32 pair tile) so each block is 16-byte aligned.
+`choose_chunks` sizes blocks to about one wave of output tiles.
 
 The GEMM itself is injected (`gemm_fn`) so the orchestration can be tested
 on CPU with the gloo backend (tests/test_dist.py).
@@ -20,7 +23,6 @@ on CPU with the gloo backend (tests/test_dist.py).
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
 
 
 def panel_bounds(M: int, world: int, rank: int) -> tuple[int, int]:
@@ -32,7 +34,7 @@ def panel_bounds(M: int, world: int, rank: int) -> tuple[int, int]:
     return r0, min(M, r0 + h)
 
 
-def chunk_bounds(N: int, chunks: int, align: int = 128) -> list[tuple[int, int]]:
+def chunk_bounds(N: int, chunks: int, align: int = 256) -> list[tuple[int, int]]:
     """Column blocks [c0, c1) covering [0, N): `chunks` blocks (fewer if N is
     small) whose widths are multiples of `align` except possibly the last."""
     if N <= 0:
@@ -46,14 +48,15 @@ def chunk_bounds(N: int, chunks: int, align: int = 128) -> list[tuple[int, int]]
     return out
 
 
-@dataclass
-class PanelTiming:
-    bcast_ms: float
-    total_ms: float
+def choose_chunks(rows: int, N: int, sms: int = 148, tile: int = 256, max_chunks: int = 8) -> int:
+    """Number of B column blocks for a rank's (rows x N) panel: about one wave of
+    256 x 256 output tiles per block on `sms` SMs (CTA pairs), at least 1."""
+    tiles = math.ceil(rows / tile) * math.ceil(N / tile)
+    return max(1, min(max_chunks, tiles // max(1, sms // 2)))
 
 
 def rowpanel_gemm(A_panel, B_blocks, C_panel, bounds, group=None, root=0, gemm_fn=None,
-                  comm_stream=None, broadcast=True):
+                  comm_stream=None, compute_streams=None, broadcast=True):
     """One distributed product step on this rank.
 
     A_panel : (rows_r, K) tensor, this rank's rows of A.
@@ -62,7 +65,9 @@ def rowpanel_gemm(A_panel, B_blocks, C_panel, bounds, group=None, root=0, gemm_f
     C_panel : (rows_r, N) row-major tensor; column block c is written by
               gemm_fn(A_panel, B_blocks[c], C_panel[:, c0:c1]).
     bounds  : chunk_bounds(N, len(B_blocks)).
-    Returns the list of per-block "arrived" events (CUDA) or None (CPU).
+    On CUDA the caller's current stream is joined to all the work before return
+    (the step is complete in stream order).  Returns the "block arrived" events
+    (CUDA) or None (CPU).
     """
     import torch
     import torch.distributed as dist
@@ -72,26 +77,34 @@ def rowpanel_gemm(A_panel, B_blocks, C_panel, bounds, group=None, root=0, gemm_f
 
         def gemm_fn(a, b, c):
             gemm_fn_default(a, b, out=c)
-    on_cuda = A_panel.is_cuda
-    events = []
-    if on_cuda:
-        compute = torch.cuda.current_stream()
-        comm = comm_stream or torch.cuda.Stream()
-        comm.wait_stream(compute)
-        for blk in B_blocks:
+    if not A_panel.is_cuda:
+        # CPU (gloo) path: same order, no overlap
+        for (c0, c1), blk in zip(bounds, B_blocks):
             if broadcast:
-                with torch.cuda.stream(comm):
-                    dist.broadcast(blk, src=root, group=group)
-            ev = torch.cuda.Event()
-            ev.record(comm)
-            events.append(ev)
-        for (c0, c1), blk, ev in zip(bounds, B_blocks, events):
-            compute.wait_event(ev)
+                dist.broadcast(blk, src=root, group=group)
             gemm_fn(A_panel, blk, C_panel[:, c0:c1])
-        return events
-    # CPU (gloo) path: same order, no overlap
-    for (c0, c1), blk in zip(bounds, B_blocks):
+        return None
+
+    caller = torch.cuda.current_stream()
+    comm = comm_stream or torch.cuda.Stream()
+    streams = compute_streams or [torch.cuda.Stream(), torch.cuda.Stream()]
+    comm.wait_stream(caller)
+    for st in streams:
+        st.wait_stream(caller)
+    events = []
+    for blk in B_blocks:
         if broadcast:
-            dist.broadcast(blk, src=root, group=group)
-        gemm_fn(A_panel, blk, C_panel[:, c0:c1])
-    return None
+            with torch.cuda.stream(comm):
+                dist.broadcast(blk, src=root, group=group)
+        ev = torch.cuda.Event()
+        ev.record(comm)
+        events.append(ev)
+    for i, ((c0, c1), blk, ev) in enumerate(zip(bounds, B_blocks, events)):
+        st = streams[i % len(streams)]
+        st.wait_event(ev)
+        with torch.cuda.stream(st):
+            gemm_fn(A_panel, blk, C_panel[:, c0:c1])
+    caller.wait_stream(comm)
+    for st in streams:
+        caller.wait_stream(st)
+    return events
