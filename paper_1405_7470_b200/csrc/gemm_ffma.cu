@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tile_coords(t, p, tm, tn);
                 const int m0 = tm * BM, n0 = tn * BN;
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_wait_sleep(&empty[stage], phase ^ 1, 2000);
                     float *sa = stages + stage * (A_TILE + B_TILE);
                     float *sb = sa + A_TILE;
                     mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_wait(&full[stage], phase);
             const float *sa = stages + stage * (A_TILE + B_TILE);
             const float *sb = sa + A_TILE;
-#pragma unroll 2
+#pragma unroll
             for (int kq = 0; kq < BK / 4; ++kq) {
                 float a[4][8], b[4][8];
                 load_a<AK>(sa, kq, wm, lm, a);

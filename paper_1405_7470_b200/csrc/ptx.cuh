@@ -44,6 +44,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+// As mbar_wait, with a suspend-time hint (ns): for a waiter that is expected to
+// wait long (a producer whose ring is full), so it sleeps instead of spinning on
+// issue slots its SM sub-partition shares with math warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t hint_ns) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n\t"
+        "DONE:\n\t"
+        "}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(hint_ns)
+        : "memory");
+}
+
 // Non-blocking: 1 if the phase with parity `parity` of `bar` has completed.
 __device__ __forceinline__ uint32_t mbar_test(uint64_t *bar, uint32_t parity) {
     uint32_t ok;
