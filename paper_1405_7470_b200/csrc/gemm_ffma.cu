@@ -33,14 +33,23 @@
 namespace lpy {
 namespace ffma {
 
-constexpr int BM = 128, BN = 128, BK = 32;
+constexpr int BN = 128, BK = 32;
 constexpr int STAGES = 4;
-constexpr int CWARPS = 8;                       // consumer warps
-constexpr int THREADS = (CWARPS + 1) * 32;      // + 1 TMA producer warp
-constexpr int A_TILE = BM * BK;                 // floats
-constexpr int B_TILE = BN * BK;
-constexpr uint32_t STAGE_BYTES = (A_TILE + B_TILE) * 4;
-constexpr size_t SMEM_BYTES = 1024 + STAGES * size_t(STAGE_BYTES) + 2 * STAGES * 8;
+
+// Per-variant geometry.  Consumer warps are laid out 4 along n (32 columns each)
+// and CWARPS/4 along m (64 rows each).  (12 warps / 192 x 128 tiles was measured
+// for the row-major layout and was slower: 55.6 vs 58 TFLOP/s, math-pipe
+// throttle instead of latency was then the top stall.)
+template <bool AK, bool BKM>
+struct Geo {
+    static constexpr int CWARPS = 8;                       // consumer warps
+    static constexpr int BM = CWARPS / 4 * 64;
+    static constexpr int THREADS = (CWARPS + 1) * 32;      // + 1 TMA producer warp
+    static constexpr int A_TILE = BM * BK;                 // floats
+    static constexpr int B_TILE = BN * BK;
+    static constexpr uint32_t STAGE_BYTES = (A_TILE + B_TILE) * 4;
+    static constexpr size_t SMEM_BYTES = 1024 + STAGES * size_t(STAGE_BYTES) + 2 * STAGES * 8;
+};
 
 struct Params {
     int M, N, K;
@@ -90,7 +99,7 @@ __device__ __forceinline__ int b_col(int wn, int ln, int j) {
 }
 
 // a[k][i] = A(tile row a_row(i), k-block column 4*kq + k)
-template <bool AK>
+template <bool AK, int BM>
 __device__ __forceinline__ void load_a(const float *sa, int kq, int wm, int lm, float (&a)[4][8]) {
     if constexpr (AK) {
         // K-major tile: row m holds BK=32 floats (128 B), 16-byte chunk c stored at c ^ (m & 7)
@@ -135,9 +144,12 @@ __device__ __forceinline__ void load_b(const float *sb, int kq, int wn, int ln, 
 }
 
 template <bool AK, bool BKM>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
     gemm_ffma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const Params p) {
+    using G = Geo<AK, BKM>;
+    constexpr int CWARPS = G::CWARPS, BM = G::BM, A_TILE = G::A_TILE, B_TILE = G::B_TILE;
+    constexpr uint32_t STAGE_BYTES = G::STAGE_BYTES;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzled K-major tiles
     const uint32_t raw = smem_u32(smem_raw);
@@ -214,10 +226,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_wait(&full[stage], phase);
             const float *sa = stages + stage * (A_TILE + B_TILE);
             const float *sb = sa + A_TILE;
-#pragma unroll
+            constexpr int UNR = (!AK && BKM) ? 2 : BK / 4;   // full unroll where registers allow
+#pragma unroll UNR
             for (int kq = 0; kq < BK / 4; ++kq) {
                 float a[4][8], b[4][8];
-                load_a<AK>(sa, kq, wm, lm, a);
+                load_a<AK, BM>(sa, kq, wm, lm, a);
                 load_b<BKM>(sb, kq, wn, ln, b);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -296,26 +309,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 template <bool AK, bool BKM>
-static cudaError_t launch_t(const CUtensorMap &ta, const CUtensorMap &tb, const Params &prm, int grid,
-                            cudaStream_t s) {
-    auto kern = gemm_ffma_kernel<AK, BKM>;
-    static bool attr_done = false;  // benign race: setting the attribute twice is harmless
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(SMEM_BYTES));
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
-    kern<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, prm);
-    return cudaGetLastError();
-}
-
-}  // namespace ffma
-
-cudaError_t launch_ffma(const Problem &p, const Knobs &kn, cudaStream_t s) {
-    using namespace ffma;
-    const bool AK = (p.la == 0);   // row-major A: K contiguous
-    const bool BKM = (p.lb == 1);  // column-major B: K contiguous
+static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
+    using G = Geo<AK, BKM>;
+    constexpr int BM = G::BM;
     CUtensorMap ta, tb;
     cudaError_t e;
     if (AK) e = make_tmap_2d(&ta, p.A, p.K, p.M, p.lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -338,10 +334,27 @@ cudaError_t launch_ffma(const Problem &p, const Knobs &kn, cudaStream_t s) {
     if (grid > prm.num_tiles) grid = prm.num_tiles;
     if (grid < 1) grid = 1;
 
-    if (AK && BKM)  return launch_t<true, true>(ta, tb, prm, grid, s);
-    if (AK && !BKM) return launch_t<true, false>(ta, tb, prm, grid, s);
-    if (!AK && BKM) return launch_t<false, true>(ta, tb, prm, grid, s);
-    return launch_t<false, false>(ta, tb, prm, grid, s);
+    auto kern = gemm_ffma_kernel<AK, BKM>;
+    static bool attr_done = false;  // benign race: setting the attribute twice is harmless
+    if (!attr_done) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::SMEM_BYTES));
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    kern<<<grid, G::THREADS, G::SMEM_BYTES, s>>>(ta, tb, prm);
+    return cudaGetLastError();
+}
+
+}  // namespace ffma
+
+cudaError_t launch_ffma(const Problem &p, const Knobs &kn, cudaStream_t s) {
+    using namespace ffma;
+    const bool AK = (p.la == 0);   // row-major A: K contiguous
+    const bool BKM = (p.lb == 1);  // column-major B: K contiguous
+    if (AK && BKM)  return launch_t<true, true>(p, kn, s);
+    if (AK && !BKM) return launch_t<true, false>(p, kn, s);
+    if (!AK && BKM) return launch_t<false, true>(p, kn, s);
+    return launch_t<false, false>(p, kn, s);
 }
 
 }  // namespace lpy
