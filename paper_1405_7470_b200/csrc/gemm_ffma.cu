@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
             mbar_wait(&full[stage], phase);
             const float *sa = stages + stage * (A_TILE + B_TILE);
             const float *sb = sa + A_TILE;
-            constexpr int UNR = (!AK && BKM) ? 2 : BK / 4;   // full unroll where registers allow
+            constexpr int UNR = BKM ? 2 : BK / 4;   // full unroll where registers allow
 #pragma unroll UNR
             for (int kq = 0; kq < BK / 4; ++kq) {
                 float a[4][8], b[4][8];
