@@ -6,8 +6,9 @@
 // tests/test_numerics_tmem.py).  So each fp32 x is used as
 //     big   = x                                  (the hardware sees trunc_tf32(x))
 //     small = rna_tf32(x - trunc_tf32(x))        (computed here; exact residual, rounded)
-// and  a*b ~= a_big*b_small + a_small*b_big + a_big*b_big  (small*small dropped;
-// the small terms go first).  Per product the representation error is below
+// and  a*b ~= a_big*b_small + a_big*b_big + a_small*b_big  (small*small dropped;
+// issued in that order so the two MMAs sharing A_big are adjacent).  Per
+// product the representation error is below
 // 2^-20 |a||b|.  TMEM accumulation rounds toward zero (measured), so the
 // accumulator is PROMOTED: every `promote` k-blocks the MMA closes a TMEM partial
 // (double-buffered, 2 x 256 columns) and the partial is added into fp32 registers
