@@ -11,21 +11,27 @@
 //     raster order so concurrently running tiles share A/B panels in L2;
 //   * split k -> (k_block, k in block), BK = 32: the "prefetch" of A[tile,kb]
 //     and B[kb,tile] is one TMA (cp.async.bulk.tensor) per operand per k-block
-//     into a 4-stage shared-memory ring guarded by full/empty mbarriers
-//     (producer warp <-> 8 consumer warps) instead of work-group barriers;
+//     into a shared-memory ring guarded by full/empty mbarriers (producer warp
+//     <-> consumer warps) instead of work-group barriers;
 //   * ilp + unr: each consumer thread owns an 8x8 register micro-tile and runs
-//     the k loop unrolled; operands come from shared memory as LDS.128
-//     fragments with in-warp broadcast (8 lanes share each A fragment, 8 each
-//     B fragment);
+//     the k loop fully unrolled; operands come from shared memory as LDS.128
+//     fragments with in-warp broadcast, and the products are packed FFMA2
+//     (fma.rn.f32x2: two fp32 RN FMAs per instruction, a scalar of A times a
+//     pair of adjacent B columns);
 //   * ragged edges: TMA zero-fills out-of-range rows/columns/k of a
 //     box, so the mainloop carries no conditionals; only the epilogue stores
 //     are predicated.
 //
-// Layouts: for each operand the tile lands in shared memory in its
-// storage orientation -- "MN-major" ([k][m] / [k][n], no swizzle) or
-// "K-major" ([m][k] / [n][k], 128-byte TMA swizzle) -- and the fragment loader
-// is specialised per orientation so every LDS.128 is bank-conflict-free.
-// Accumulation is fp32 FFMA (RN) with k ascending per element.
+// Layouts.  The consumers always read both operands "MN-major"
+// ([k][m] and [k][n]: 4 adjacent rows / columns per LDS.128), the orientation
+// whose fragments feed FFMA2 without any register repacking.  An operand
+// stored K-major (row-major A, column-major B) lands from TMA as [m][k] /
+// [n][k] with the 128-byte swizzle, and three "transpose" warps rewrite each
+// such tile into an MN-major copy (4x4 register transposes, bank-conflict-free
+// on both sides) -- the paper's "precompute" into local temporaries
+// used as a layout change -- before the consumers see it.
+// Accumulation is fp32 FFMA (RN) with k ascending per element, identical for
+// every layout.
 #include <cstdio>
 #include "lpy_internal.h"
 #include "ptx.cuh"
@@ -33,23 +39,29 @@
 namespace lpy {
 namespace ffma {
 
-constexpr int BN = 128, BK = 32;   // (BK = 64 with 3 stages measured no faster: 57.7 vs 58.0 TFLOP/s)
-constexpr int KSUB = 32;                        // k per 128B-swizzled K-major sub-tile
-constexpr int STAGES = 4;
+constexpr int BM = 128, BN = 128, BK = 32;   // (BK = 64 with 3 stages measured no faster)
+constexpr int KSUB = 32;                     // k per 128B-swizzled K-major TMA box (= BK)
+constexpr int CWARPS = 8;                    // consumer warps: 2 along m (64 rows) x 4 along n (32 cols)
+constexpr int XWARPS = 3;                    // transpose warps (warps CWARPS+1 .. CWARPS+3)
 
-// Per-variant geometry.  Consumer warps are laid out 4 along n (32 columns each)
-// and CWARPS/4 along m (64 rows each).  (12 warps / 192 x 128 tiles was measured
-// for the row-major layout and was slower: 55.6 vs 58 TFLOP/s, math-pipe
-// throttle instead of latency was then the top stall.)
+// Per-layout geometry.  AK: A is K-major (row-major A); BKM: B is K-major
+// (column-major B).  Each stage holds the raw TMA tiles plus MN-major copies
+// of the K-major ones.
 template <bool AK, bool BKM>
 struct Geo {
-    static constexpr int CWARPS = 8;                       // consumer warps
-    static constexpr int BM = CWARPS / 4 * 64;
-    static constexpr int THREADS = (CWARPS + 1) * 32;      // + 1 TMA producer warp
-    static constexpr int A_TILE = BM * BK;                 // floats
-    static constexpr int B_TILE = BN * BK;
-    static constexpr uint32_t STAGE_BYTES = (A_TILE + B_TILE) * 4;
-    static constexpr size_t SMEM_BYTES = 1024 + STAGES * size_t(STAGE_BYTES) + 2 * STAGES * 8;
+    static constexpr bool XA = AK, XB = BKM, X = AK || BKM;
+    static constexpr int STAGES = (AK && BKM) ? 3 : 4;
+    // 8 consumer warps + a producer warpgroup (warp CWARPS: one TMA lane; the next
+    // XWARPS warps: transposes).  A whole warpgroup so setmaxnreg can move its
+    // registers to the consumers: launched at 168/thread (the SMSP holding 3
+    // warps caps a 12-warp CTA there), consumers rise to REGS_CONS, the producer
+    // group drops to REGS_PROD (2*32*224 + 32*56 <= 16384 per SMSP).
+    static constexpr int THREADS = (CWARPS + 4) * 32;
+    static constexpr int REGS_CONS = 224, REGS_PROD = 56;
+    static constexpr int A_TILE = BM * BK, B_TILE = BN * BK;   // floats
+    static constexpr int STAGE_FLOATS = A_TILE + B_TILE + (XA ? A_TILE : 0) + (XB ? B_TILE : 0);
+    static constexpr uint32_t TMA_BYTES = (A_TILE + B_TILE) * 4;
+    static constexpr size_t SMEM_BYTES = 1024 + STAGES * size_t(STAGE_FLOATS) * 4 + 3 * STAGES * 8;
 };
 
 struct Params {
@@ -89,61 +101,55 @@ __device__ __forceinline__ void tile_coords(int t, const Params &p, int &tm, int
     tn = r / gsize;
 }
 
-// Row (within the 128-row tile) of this thread's i-th accumulator row.
-template <bool AK>
-__device__ __forceinline__ int a_row(int wm, int lm, int i) {
-    return AK ? wm * 64 + lm + 8 * i : wm * 64 + (i >> 2) * 32 + lm * 4 + (i & 3);
-}
-template <bool BKM>
-__device__ __forceinline__ int b_col(int wn, int ln, int j) {
-    return BKM ? wn * 32 + ln + 4 * j : wn * 32 + (j >> 2) * 16 + ln * 4 + (j & 3);
-}
+// Row (within the tile) of this thread's i-th accumulator row, column of its j-th.
+__device__ __forceinline__ int a_row(int wm, int lm, int i) { return wm * 64 + (i >> 2) * 32 + lm * 4 + (i & 3); }
+__device__ __forceinline__ int b_col(int wn, int ln, int j) { return wn * 32 + (j >> 2) * 16 + ln * 4 + (j & 3); }
 
-// a[k][i] = A(tile row a_row(i), k-block column 4*kq + k)
-template <bool AK, int BM>
+// a[k][i] = A(a_row(i), 4*kq + k) from an MN-major [BK][BM] tile.
 __device__ __forceinline__ void load_a(const float *sa, int kq, int wm, int lm, float (&a)[4][8]) {
-    if constexpr (AK) {
-        // K-major tile: BK/KSUB sub-tiles of BM rows x 32 floats (128 B); 16-byte chunk c of
-        // row m stored at c ^ (m & 7)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int m = wm * 64 + lm + 8 * i;
-            const float4 v = *reinterpret_cast<const float4 *>(sa + (kq >> 3) * BM * KSUB + m * KSUB +
-                                                                ((((kq & 7) ^ (m & 7))) << 2));
-            a[0][i] = v.x; a[1][i] = v.y; a[2][i] = v.z; a[3][i] = v.w;
-        }
-    } else {
-        // MN-major tile: k-row holds BM=128 floats
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float *row = sa + (kq * 4 + k) * BM + wm * 64 + lm * 4;
-            const float4 v0 = *reinterpret_cast<const float4 *>(row);
-            const float4 v1 = *reinterpret_cast<const float4 *>(row + 32);
-            a[k][0] = v0.x; a[k][1] = v0.y; a[k][2] = v0.z; a[k][3] = v0.w;
-            a[k][4] = v1.x; a[k][5] = v1.y; a[k][6] = v1.z; a[k][7] = v1.w;
-        }
+    for (int k = 0; k < 4; ++k) {
+        const float *row = sa + (kq * 4 + k) * BM + wm * 64 + lm * 4;
+        const float4 v0 = *reinterpret_cast<const float4 *>(row);
+        const float4 v1 = *reinterpret_cast<const float4 *>(row + 32);
+        a[k][0] = v0.x; a[k][1] = v0.y; a[k][2] = v0.z; a[k][3] = v0.w;
+        a[k][4] = v1.x; a[k][5] = v1.y; a[k][6] = v1.z; a[k][7] = v1.w;
     }
 }
 
-template <bool BKM>
+// b[k][j] = B(4*kq + k, b_col(j)) from an MN-major [BK][BN] tile.
 __device__ __forceinline__ void load_b(const float *sb, int kq, int wn, int ln, float (&b)[4][8]) {
-    if constexpr (BKM) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int n = wn * 32 + ln + 4 * j;
-            const float4 v = *reinterpret_cast<const float4 *>(sb + (kq >> 3) * BN * KSUB + n * KSUB +
-                                                                ((((kq & 7) ^ (n & 7))) << 2));
-            b[0][j] = v.x; b[1][j] = v.y; b[2][j] = v.z; b[3][j] = v.w;
-        }
-    } else {
+    for (int k = 0; k < 4; ++k) {
+        const float *row = sb + (kq * 4 + k) * BN + wn * 32 + ln * 4;
+        const float4 v0 = *reinterpret_cast<const float4 *>(row);
+        const float4 v1 = *reinterpret_cast<const float4 *>(row + 16);
+        b[k][0] = v0.x; b[k][1] = v0.y; b[k][2] = v0.z; b[k][3] = v0.w;
+        b[k][4] = v1.x; b[k][5] = v1.y; b[k][6] = v1.z; b[k][7] = v1.w;
+    }
+}
+
+// K-major tile (128 lines x 32 k, TMA 128B swizzle: 16-byte chunk c of line r
+// stored at chunk c ^ (r & 7)) -> MN-major [32 k][128] copy.  The tile is 8
+// k-chunks x 32 line-groups of 4x4 blocks; one warp pass covers 4 chunks x 8
+// line-groups (lane = chunk + 4 * group), so both the four LDS.128 (8 distinct
+// swizzled chunks per 128 B row pair) and the four STS.128 (8 distinct groups
+// per k row) move 512 B in 4 wavefronts, the minimum.
+__device__ __forceinline__ void transpose_tile(const float *src, float *dst, int xw, int lane) {
+    for (int it = xw; it < 8; it += XWARPS) {
+        const int c = (it & 1) * 4 + (lane & 3);
+        const int g = (it >> 1) * 8 + (lane >> 2);
+        float4 r[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float *row = sb + (kq * 4 + k) * BN + wn * 32 + ln * 4;
-            const float4 v0 = *reinterpret_cast<const float4 *>(row);
-            const float4 v1 = *reinterpret_cast<const float4 *>(row + 16);
-            b[k][0] = v0.x; b[k][1] = v0.y; b[k][2] = v0.z; b[k][3] = v0.w;
-            b[k][4] = v1.x; b[k][5] = v1.y; b[k][6] = v1.z; b[k][7] = v1.w;
+        for (int q = 0; q < 4; ++q) {
+            const int line = 4 * g + q;
+            r[q] = *reinterpret_cast<const float4 *>(src + line * KSUB + ((c ^ (line & 7)) << 2));
         }
+        float *d = dst + (4 * c) * 128 + 4 * g;
+        *reinterpret_cast<float4 *>(d + 0 * 128) = make_float4(r[0].x, r[1].x, r[2].x, r[3].x);
+        *reinterpret_cast<float4 *>(d + 1 * 128) = make_float4(r[0].y, r[1].y, r[2].y, r[3].y);
+        *reinterpret_cast<float4 *>(d + 2 * 128) = make_float4(r[0].z, r[1].z, r[2].z, r[3].z);
+        *reinterpret_cast<float4 *>(d + 3 * 128) = make_float4(r[0].w, r[1].w, r[2].w, r[3].w);
     }
 }
 
@@ -152,14 +158,19 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
     gemm_ffma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const Params p) {
     using G = Geo<AK, BKM>;
-    constexpr int CWARPS = G::CWARPS, BM = G::BM, A_TILE = G::A_TILE, B_TILE = G::B_TILE;
-    constexpr uint32_t STAGE_BYTES = G::STAGE_BYTES;
+    constexpr int STAGES = G::STAGES, A_TILE = G::A_TILE, B_TILE = G::B_TILE, SF = G::STAGE_FLOATS;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzled K-major tiles
     const uint32_t raw = smem_u32(smem_raw);
     float *stages = reinterpret_cast<float *>(smem_raw + (((raw + 1023) & ~1023u) - raw));
-    uint64_t *full = reinterpret_cast<uint64_t *>(stages + STAGES * (A_TILE + B_TILE));
-    uint64_t *empty = full + STAGES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(stages + STAGES * SF);  // TMA landed
+    uint64_t *xfull = full + STAGES;                                      // transposes written
+    uint64_t *empty = xfull + STAGES;                                     // stage free again
+    // stage s: [raw A][raw B][MN-major A if AK][MN-major B if BKM]
+    auto raw_a = [&](int s) { return stages + s * SF; };
+    auto raw_b = [&](int s) { return stages + s * SF + A_TILE; };
+    auto x_a = [&](int s) { return stages + s * SF + A_TILE + B_TILE; };
+    auto x_b = [&](int s) { return stages + s * SF + A_TILE + B_TILE + (G::XA ? A_TILE : 0); };
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -167,42 +178,50 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], CWARPS);
+            mbar_init(&xfull[s], XWARPS * 32);
+            mbar_init(&empty[s], CWARPS + (G::X ? XWARPS : 0));
         }
         fence_mbar_init();
     }
     __syncthreads();
 
-    if (warp == CWARPS) {
-        // ------------------------------------------------ TMA producer
-        if (lane == 0) {
-            tma_prefetch_desc(&tmA);
-            tma_prefetch_desc(&tmB);
+    if (warp >= CWARPS) {
+        setmaxnreg_dec<G::REGS_PROD>();
+        if (warp == CWARPS) {
+            // -------------------------------------------- TMA producer
+            if (lane == 0) {
+                tma_prefetch_desc(&tmA);
+                tma_prefetch_desc(&tmB);
+                int stage = 0;
+                uint32_t phase = 0;
+                for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                    int tm, tn;
+                    tile_coords(t, p, tm, tn);
+                    const int m0 = tm * BM, n0 = tn * BN;
+                    for (int kb = 0; kb < p.k_blocks; ++kb) {
+                        mbar_wait_sleep(&empty[stage], phase ^ 1, 2000);
+                        mbar_arrive_expect_tx(&full[stage], G::TMA_BYTES);
+                        if constexpr (AK) tma_load_2d(raw_a(stage), &tmA, &full[stage], kb * BK, m0);
+                        else              tma_load_2d(raw_a(stage), &tmA, &full[stage], m0, kb * BK);
+                        if constexpr (BKM) tma_load_2d(raw_b(stage), &tmB, &full[stage], kb * BK, n0);
+                        else               tma_load_2d(raw_b(stage), &tmB, &full[stage], n0, kb * BK);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        } else if constexpr (G::X) {
+            // -------------------------------------------- transposes of K-major tiles
+            const int xw = warp - CWARPS - 1;
             int stage = 0;
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-                int tm, tn;
-                tile_coords(t, p, tm, tn);
-                const int m0 = tm * BM, n0 = tn * BN;
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
-                    mbar_wait_sleep(&empty[stage], phase ^ 1, 2000);
-                    float *sa = stages + stage * (A_TILE + B_TILE);
-                    float *sb = sa + A_TILE;
-                    mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-                    if constexpr (AK) {
-#pragma unroll
-                        for (int j = 0; j < BK / KSUB; ++j)
-                            tma_load_2d(sa + j * BM * KSUB, &tmA, &full[stage], kb * BK + j * KSUB, m0);
-                    } else {
-                        tma_load_2d(sa, &tmA, &full[stage], m0, kb * BK);
-                    }
-                    if constexpr (BKM) {
-#pragma unroll
-                        for (int j = 0; j < BK / KSUB; ++j)
-                            tma_load_2d(sb + j * BN * KSUB, &tmB, &full[stage], kb * BK + j * KSUB, n0);
-                    } else {
-                        tma_load_2d(sb, &tmB, &full[stage], n0, kb * BK);
-                    }
+                    mbar_wait(&full[stage], phase);
+                    if constexpr (G::XA) transpose_tile(raw_a(stage), x_a(stage), xw, lane);
+                    if constexpr (G::XB) transpose_tile(raw_b(stage), x_b(stage), xw, lane);
+                    mbar_arrive(&xfull[stage]);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -211,6 +230,7 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
     }
 
     // ---------------------------------------------------- consumers
+    setmaxnreg_inc<G::REGS_CONS>();
     const int wm = warp >> 2, wn = warp & 3;
     const int lm = lane >> 2, ln = lane & 3;
     int stage = 0;
@@ -218,58 +238,33 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         int tm, tn;
         tile_coords(t, p, tm, tn);
-        // Accumulators as packed pairs for FFMA2, paired along the operand whose
-        // fragment arrives with adjacent elements from one LDS.128:
-        //   PAIR_J (B MN-major): acc2[i][jp] = (acc(i, 2jp), acc(i, 2jp+1)), a broadcast
-        //   PAIR_I (A MN-major, B K-major): acc2[ip][j] = (acc(2ip, j), acc(2ip+1, j)), b broadcast
-        // Both K-major: plain FFMA (pairing would cost a register move per FFMA2).
-        constexpr bool PAIR_J = !BKM, PAIR_I = BKM && !AK;
-        constexpr int P0 = PAIR_I ? 4 : 8, P1 = PAIR_I ? 8 : 4;
-        unsigned long long acc2[P0][P1];
-        float accf[8][8];
-#pragma unroll
-        for (int i = 0; i < P0; ++i)
-#pragma unroll
-            for (int j = 0; j < P1; ++j) acc2[i][j] = 0ull;
+        // acc2[i][jp] = (acc(i, 2jp), acc(i, 2jp+1)): pairs along n, where one
+        // LDS.128 of the MN-major B tile delivers adjacent columns
+        unsigned long long acc2[8][4];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) accf[i][j] = 0.f;
+            for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
 
         for (int kb = 0; kb < p.k_blocks; ++kb) {
-            mbar_wait(&full[stage], phase);
-            const float *sa = stages + stage * (A_TILE + B_TILE);
-            const float *sb = sa + A_TILE;
-            constexpr int UNR = BKM ? 2 : 8;   // deep unroll where registers allow
-#pragma unroll UNR
+            if constexpr (!(G::XA && G::XB)) mbar_wait(&full[stage], phase);   // reads a raw tile
+            if constexpr (G::X) mbar_wait(&xfull[stage], phase);
+            const float *sa = G::XA ? x_a(stage) : raw_a(stage);
+            const float *sb = G::XB ? x_b(stage) : raw_b(stage);
+#pragma unroll
             for (int kq = 0; kq < BK / 4; ++kq) {
                 float a[4][8], b[4][8];
-                load_a<AK, BM>(sa, kq, wm, lm, a);
-                load_b<BKM>(sb, kq, wn, ln, b);
+                load_a(sa, kq, wm, lm, a);
+                load_b(sb, kq, wn, ln, b);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    if constexpr (PAIR_J) {
-                        unsigned long long bp[4];   // adjacent registers: packing is free
+                    unsigned long long bp[4];   // adjacent registers: packing is free
 #pragma unroll
-                        for (int jp = 0; jp < 4; ++jp) bp[jp] = pack2(b[k][2 * jp], b[k][2 * jp + 1]);
+                    for (int jp = 0; jp < 4; ++jp) bp[jp] = pack2(b[k][2 * jp], b[k][2 * jp + 1]);
 #pragma unroll
-                        for (int i = 0; i < 8; ++i)
+                    for (int i = 0; i < 8; ++i)
 #pragma unroll
-                            for (int jp = 0; jp < 4; ++jp) ffma2(acc2[i][jp], a[k][i], bp[jp]);
-                    } else if constexpr (PAIR_I) {
-                        unsigned long long ap[4];
-#pragma unroll
-                        for (int ip = 0; ip < 4; ++ip) ap[ip] = pack2(a[k][2 * ip], a[k][2 * ip + 1]);
-#pragma unroll
-                        for (int ip = 0; ip < 4; ++ip)
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) ffma2(acc2[ip][j], b[k][j], ap[ip]);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) accf[i][j] = fmaf(a[k][i], b[k][j], accf[i][j]);
-                    }
+                        for (int jp = 0; jp < 4; ++jp) ffma2(acc2[i][jp], a[k][i], bp[jp]);
                 }
             }
             __syncwarp();
@@ -278,44 +273,25 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
         }
 
         // ------------------------------------------------ epilogue (ragged-edge stores)
-        float acc[8][8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if constexpr (PAIR_J) {
-                    if (j % 2 == 0) unpack2(acc2[i][j / 2], acc[i][j], acc[i][j + 1]);
-                } else if constexpr (PAIR_I) {
-                    if (i % 2 == 0) unpack2(acc2[i / 2][j], acc[i][j], acc[i + 1][j]);
-                } else {
-                    acc[i][j] = accf[i][j];
-                }
-            }
         const int m0 = tm * BM, n0 = tn * BN;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int row = m0 + a_row<AK>(wm, lm, i);
+            const int row = m0 + a_row(wm, lm, i);
             if (row >= p.M) continue;
+            float acc[8];
+#pragma unroll
+            for (int jp = 0; jp < 4; ++jp) unpack2(acc2[i][jp], acc[2 * jp], acc[2 * jp + 1]);
             float *crow = p.C + int64_t(row) * p.ldc;
-            if constexpr (!BKM) {
 #pragma unroll
-                for (int jq = 0; jq < 2; ++jq) {
-                    const int col = n0 + b_col<BKM>(wn, ln, jq * 4);
-                    if (p.c_vec && col + 3 < p.N) {
-                        *reinterpret_cast<float4 *>(crow + col) =
-                            make_float4(acc[i][jq * 4 + 0], acc[i][jq * 4 + 1], acc[i][jq * 4 + 2],
-                                        acc[i][jq * 4 + 3]);
-                    } else {
+            for (int jq = 0; jq < 2; ++jq) {
+                const int col = n0 + b_col(wn, ln, jq * 4);
+                if (p.c_vec && col + 3 < p.N) {
+                    *reinterpret_cast<float4 *>(crow + col) =
+                        make_float4(acc[jq * 4 + 0], acc[jq * 4 + 1], acc[jq * 4 + 2], acc[jq * 4 + 3]);
+                } else {
 #pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            if (col + e < p.N) crow[col + e] = acc[i][jq * 4 + e];
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int col = n0 + b_col<BKM>(wn, ln, j);
-                    if (col < p.N) crow[col] = acc[i][j];
+                    for (int e = 0; e < 4; ++e)
+                        if (col + e < p.N) crow[col + e] = acc[jq * 4 + e];
                 }
             }
         }
@@ -325,7 +301,6 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
 template <bool AK, bool BKM>
 static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     using G = Geo<AK, BKM>;
-    constexpr int BM = G::BM;
     CUtensorMap ta, tb;
     cudaError_t e;
     if (AK) e = make_tmap_2d(&ta, p.A, p.K, p.M, p.lda, KSUB, BM, CU_TENSOR_MAP_SWIZZLE_128B);

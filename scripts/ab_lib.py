@@ -4,6 +4,7 @@ path (row-major, device-resident inputs, CUDA events, median of rounds) and
 check a sample of the result against the default library's.
 
 usage: python scripts/ab_lib.py <path> <n> lib1.so [lib2.so ...]
+env LA / LB = row|col pick the A / B layouts (default row).
 """
 import ctypes
 import os
@@ -20,8 +21,12 @@ import paper_1405_7470_b200 as lpy  # noqa: E402
 path, n, libs = sys.argv[1], int(sys.argv[2]), sys.argv[3:]
 A = torch.randn(n, n, device="cuda")
 B = torch.randn(n, n, device="cuda")
+if os.environ.get("LA", "row") == "col":
+    A = A.t().contiguous().t()
+if os.environ.get("LB", "row") == "col":
+    B = B.t().contiguous().t()
 results = {}
-for rnd in range(3):
+for rnd in range(int(os.environ.get("ROUNDS", "3"))):
     for lib in libs:
         lpy._lib = None
         lpy.library_path = (lambda p: (lambda: p))(os.path.abspath(lib))
