@@ -380,6 +380,58 @@ def time_e2e(args, path, rank, world, device):
             "d2h_bytes_per_step": d2h, "ms_per_step": ms}
 
 
+def time_saxpy(args, device):
+    """Table 1's saxpy row: y := alpha*x + y over n = 2^28
+    fp32 elements (1 GiB per vector, 3 GiB of HBM traffic per call, far above
+    L2) through lpy_saxpy_f32, device-resident; GB/s = 12 n / kernel time."""
+    import numpy as np
+    import torch
+    import oracle
+    import paper_1405_7470_b200 as lpy
+    n = args.saxpy_n
+    alpha = 1.5
+    g = torch.Generator(device=device)
+    g.manual_seed(0)
+    x = torch.rand(n, device=device, generator=g) * 2 - 1
+    y = torch.rand(n, device=device, generator=g) * 2 - 1
+    # parity on this launch configuration: one call on a copy, sampled elements vs the oracle
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.integers(0, n, 1 << 16))
+    ti = torch.from_numpy(idx).to(device)
+    xs, ys = x[ti].cpu().numpy(), y[ti].cpu().numpy()
+    y1 = y.clone()
+    lpy.saxpy(alpha, x, y1)
+    got = y1[ti].cpu().numpy()
+    ref = oracle.saxpy(idx.size, alpha, xs, 1, ys, 1)
+    ulps = oracle.saxpy_error_ulps(got, ref)
+    del y1
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        lpy.saxpy(alpha, x, y)
+    torch.cuda.synchronize()
+    per = []
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            lpy.saxpy(alpha, x, y)
+            e1.record(stream)
+            per.append((e0, e1))
+        torch.cuda.synchronize()
+    ms = statistics.mean(a.elapsed_time(b) for a, b in per)
+    gbs = 12.0 * n / (ms * 1e-3) / 1e9
+    peaks, src = load_peaks()
+    peak = peaks["hbm_gbs"]
+    traffic, tsrc = profile_traffic("saxpy", n)
+    return {"metric": "saxpy GB/s (y := alpha*x + y, 12 B per element)", "value": round(gbs, 1),
+            "unit": "GB/s", "n": n, "ms_per_call": round(ms, 4), "calls": args.steps, "gpu_launches": args.steps,
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbs / peak, 4), "traffic": traffic, "traffic_source": tsrc,
+                         "algorithmic_bytes": 12 * n, "peak_note": f"{src} copy bandwidth (MEASURED_PEAKS.json)"},
+            "parity_sampled_max_half_ulps": ulps, "clocks": clk.summary(),
+            "data": "synthetic: torch.rand seeded 0, uniform[-1,1), alpha = 1.5"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -398,6 +450,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--saxpy-n", type=int, default=1 << 28, help="saxpy length (0 = skip the saxpy line)")
     args = ap.parse_args()
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
 
@@ -432,6 +485,7 @@ def main():
     if args.also and args.also != main_path:
         also = time_path(args, args.also, rank, world, device, dist_on)
     e2e = None if args.no_e2e else time_e2e(args, main_path, rank, world, device)
+    sax = time_saxpy(args, device) if (args.saxpy_n > 0 and rank == 0 and not dist_on) else None
 
     if rank == 0:
         n = args.n
@@ -476,6 +530,8 @@ def main():
         }
         if dist_on:
             line["multi_gpu"] = res["multi"]
+        if sax is not None:
+            line["saxpy"] = sax
         if also is not None:
             ams = also["total_ms"] / args.steps
             line["alt_path"] = {"path": also["path"], "value": round(flops / (ams * 1e-3) / 1e9, 1),

@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define LPY_VERSION 1
+#define LPY_VERSION 2
 
 typedef enum { LPY_ROW_MAJOR = 0, LPY_COL_MAJOR = 1 } lpy_layout;
 
@@ -122,6 +122,30 @@ lpy_status lpy_gemm_f32_host(int64_t M, int64_t N, int64_t K,
                              const float *B, int64_t ldb, lpy_layout layout_b,
                              float *C, int64_t ldc, lpy_layout layout_c,
                              void *stream, lpy_path path);
+
+/* ---------------------------------------------------------------- saxpy
+ * y := alpha * x + y over n elements: Table 1's "saxpy" row (section 3),
+ * the paper's bandwidth-bound BLAS-1 workload, through the same boundary.
+ * Element i lives at x[i*incx] and y[i*incy] (incx, incy >= 1, in ELEMENTS).
+ * Each result is fl32(alpha*x_i + y_i) rounded ONCE (one fused multiply-add,
+ * round-to-nearest-even); inputs finite (reading S1).
+ * x and y are device memory of the current device, owned by the caller; y is
+ * overwritten in place, nothing else is written.  x and y must either not
+ * overlap or be the same vector (x == y, incx == incy: y := alpha*y + y);
+ * any other overlap is LPY_ERR_ALIAS.  n == 0 is a no-op.  Enqueued on
+ * `stream` (NULL = legacy default stream), asynchronous like lpy_gemm_f32.
+ * Errors: LPY_ERR_INVALID_VALUE (n < 0, inc < 1, n*inc beyond 2^62),
+ * LPY_ERR_NULL_POINTER, LPY_ERR_MISALIGNED (not 4-byte aligned), LPY_ERR_ALIAS,
+ * LPY_ERR_UNSUPPORTED_DEVICE, LPY_ERR_CUDA; validated before anything runs. */
+lpy_status lpy_saxpy_f32(int64_t n, float alpha, const float *x, int64_t incx, float *y,
+                         int64_t incy, void *stream);
+
+/* End-to-end saxpy on HOST buffers: copies x and y to device scratch, runs
+ * lpy_saxpy_f32, copies y back and SYNCHRONISES `stream` before returning.
+ * Same argument rules as lpy_saxpy_f32 (pinned host memory for full PCIe
+ * bandwidth). */
+lpy_status lpy_saxpy_f32_host(int64_t n, float alpha, const float *x, int64_t incx, float *y,
+                              int64_t incy, void *stream);
 
 /* Host-only: the path `requested` resolves to for this problem shape (no CUDA
  * calls).  Returns LPY_ERR_INVALID_VALUE for bad enum/sizes. */

@@ -48,6 +48,8 @@ def _load():
             lib.lpy_oracle_gemm_elems_f64.argtypes = [i64, i64, i64, fp, i64, i32, fp, i64, i32,
                                                       i64, fp, fp, dp, dp, i32]
             lib.lpy_oracle_gemm_elems_f64.restype = i32
+            lib.lpy_oracle_saxpy_f64.argtypes = [i64, ctypes.c_float, fp, i64, fp, i64, dp, i32]
+            lib.lpy_oracle_saxpy_f64.restype = i32
             lib.lpy_oracle_max_threads.argtypes = []
             lib.lpy_oracle_max_threads.restype = i32
             _lib = lib
@@ -96,6 +98,40 @@ def gemm_elems(M, N, K, A, lda, la, B, ldb, lb, ii, jj, nthreads=0):
     if rc != 0:
         raise ValueError("oracle rejected its arguments")
     return C, D
+
+
+def saxpy(n, alpha, x, incx, y, incy, nthreads=0):
+    """float64 values of alpha*x_i + y_i, i < n (Table 1 saxpy); x, y
+    contiguous float32 buffers holding the strided vectors (only read)."""
+    _check_buf(x)
+    _check_buf(y)
+    if n > 0 and (x.size < (n - 1) * incx + 1 or y.size < (n - 1) * incy + 1):
+        raise ValueError("buffer shorter than the strided vector")
+    out = np.empty(max(n, 0), dtype=np.float64)
+    rc = _load().lpy_oracle_saxpy_f64(n, float(alpha), _ptr(x), incx, _ptr(y), incy, _ptr(out),
+                                       int(nthreads))
+    if rc != 0:
+        raise ValueError("oracle rejected its arguments")
+    return out
+
+
+def saxpy_error_ulps(y32, ref64):
+    """max |y - ref| in units of half an fp32 ulp of ref (<= 1 means y is the
+    round-to-nearest of ref up to ref's own 2^-53 relative error).  Inputs are
+    normal numbers or zeros (reading S1)."""
+    y = np.asarray(y32, dtype=np.float64)
+    ref = np.asarray(ref64, dtype=np.float64)
+    if y.size == 0:
+        return 0.0
+    # half-ulp of the fp32 binade containing |ref|: 2^(floor(log2|ref|) - 24)
+    mag = np.abs(ref)
+    e = np.where(mag > 0, np.floor(np.log2(np.where(mag > 0, mag, 1.0))), -126.0)
+    e = np.maximum(e, -126.0)                                    # subnormal spacing floor
+    half = np.ldexp(1.0, (e - 24).astype(np.int64))          # 2^-150 at and below the subnormals
+    # allow ref's own float64 rounding (<= 2^-53 |ref|)
+    r = np.abs(y - ref) / (half + np.ldexp(mag, -52))
+    r = np.where(np.isnan(y), np.inf, r)
+    return float(r.max())
 
 
 def max_threads() -> int:

@@ -7,7 +7,8 @@
  * product path (paper_1405_7470_b200/) never links, imports or executes it,
  * and this file shares no code, header, table or helper with the CUDA side.
  *
- * What it computes (section 2.1, the reduction example):
+ * What it computes (section 2.1, the reduction example;
+ * and, at the end of this file, Table 1's saxpy):
  *
  *     c[i,j] = sum(k, a[i,k]*b[k,j])
  *
@@ -124,6 +125,28 @@ int lpy_oracle_gemm_elems_f64(int64_t M, int64_t N, int64_t K,
         C[e] = c;
         if (D) D[e] = d;
     }
+    (void)nthreads;
+    return 0;
+}
+
+/* ------------------------------------------------------------------ saxpy
+ * Table 1's "saxpy" row (section 3): y := alpha * x + y.
+ * out[i] = (double)alpha * (double)x[i*incx] + (double)y[i*incy] for i < n,
+ * in float64: the product of two fp32 values is exact in float64 and the sum
+ * rounds once (relative error <= 2^-53), so `out` is the exact value of
+ * alpha*x_i + y_i for the parity contract (the fp32 result must be its
+ * round-to-nearest, reading S1).  x and y are only read; returns 0,
+ * or -1 on bad arguments (n < 0, inc < 1). */
+int lpy_oracle_saxpy_f64(int64_t n, float alpha, const float *x, int64_t incx,
+                         const float *y, int64_t incy, double *out, int nthreads)
+{
+    if (n < 0 || incx < 1 || incy < 1) return -1;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(static) num_threads(nthreads)
+#endif
+    for (int64_t i = 0; i < n; ++i)
+        out[i] = (double)alpha * (double)x[i * incx] + (double)y[i * incy];
     (void)nthreads;
     return 0;
 }

@@ -24,7 +24,8 @@ __all__ = [
     "ROW_MAJOR", "COL_MAJOR", "PATH_AUTO", "PATH_FFMA", "PATH_3XTF32", "PATHS", "LpyError",
     "GemmOpts", "library_path", "load_library", "lpy_gemm_f32", "lpy_gemm_f32_ex",
     "lpy_gemm_f32_host", "lpy_select_path", "lpy_status_string", "lpy_last_cuda_error",
-    "lpy_version", "gemm", "operand_layout", "gemm_host",
+    "lpy_version", "gemm", "operand_layout", "gemm_host", "lpy_saxpy_f32", "lpy_saxpy_f32_host",
+    "saxpy", "saxpy_host",
 ]
 
 ROW_MAJOR = 0
@@ -82,6 +83,11 @@ def load_library():
         lib.lpy_status_string.restype = ctypes.c_char_p
         lib.lpy_last_cuda_error.argtypes = []
         lib.lpy_last_cuda_error.restype = i32
+        saxpy_args = [i64, ctypes.c_float, vp, i64, vp, i64, vp]
+        lib.lpy_saxpy_f32.argtypes = saxpy_args
+        lib.lpy_saxpy_f32.restype = i32
+        lib.lpy_saxpy_f32_host.argtypes = saxpy_args
+        lib.lpy_saxpy_f32_host.restype = i32
         lib.lpy_version.argtypes = []
         lib.lpy_version.restype = i32
         _lib = lib
@@ -111,6 +117,14 @@ def lpy_select_path(M, N, K, requested=PATH_AUTO) -> tuple[int, int]:
     out = ctypes.c_int(0)
     st = load_library().lpy_select_path(M, N, K, requested, ctypes.byref(out))
     return st, out.value
+
+
+def lpy_saxpy_f32(n, alpha, x, incx, y, incy, stream=None) -> int:
+    return load_library().lpy_saxpy_f32(n, alpha, x, incx, y, incy, stream)
+
+
+def lpy_saxpy_f32_host(n, alpha, x, incx, y, incy, stream=None) -> int:
+    return load_library().lpy_saxpy_f32_host(n, alpha, x, incx, y, incy, stream)
 
 
 def lpy_status_string(status: int) -> str:
@@ -197,3 +211,41 @@ def gemm_host(M, N, K, A, lda, la, B, ldb, lb, C, ldc, lc, path="auto", stream=N
     if st != 0:
         raise LpyError(st, "lpy_gemm_f32_host")
     return C
+
+
+def _vec(v, name):
+    import torch
+    if v.dtype != torch.float32 or v.dim() != 1:
+        raise TypeError(f"{name} must be a 1-D fp32 tensor")
+    inc = v.stride(0) if v.shape[0] > 1 else 1
+    if inc < 1:
+        raise ValueError(f"{name} needs a positive stride")
+    return inc
+
+
+def saxpy(alpha, x, y, stream=None):
+    """y := alpha * x + y in place on 1-D fp32 CUDA tensors (any positive
+    stride) through lpy_saxpy_f32 -- Table 1's saxpy."""
+    if x.shape != y.shape:
+        raise ValueError("x and y must have the same length")
+    if not (x.is_cuda and y.is_cuda):
+        raise ValueError("device tensors required (use saxpy_host for host buffers)")
+    incx, incy = _vec(x, "x"), _vec(y, "y")
+    st = lpy_saxpy_f32(x.shape[0], float(alpha), x.data_ptr(), incx, y.data_ptr(), incy,
+                       _stream_handle(stream))
+    if st != 0:
+        raise LpyError(st, "lpy_saxpy_f32")
+    return y
+
+
+def saxpy_host(alpha, x, y, stream=None):
+    """End-to-end saxpy on host buffers (1-D fp32 CPU tensors, ideally pinned):
+    copies in, computes, copies y back, synchronises (lpy_saxpy_f32_host)."""
+    if x.shape != y.shape:
+        raise ValueError("x and y must have the same length")
+    incx, incy = _vec(x, "x"), _vec(y, "y")
+    st = lpy_saxpy_f32_host(x.shape[0], float(alpha), x.data_ptr(), incx, y.data_ptr(), incy,
+                            _stream_handle(stream) if stream is not None else None)
+    if st != 0:
+        raise LpyError(st, "lpy_saxpy_f32_host")
+    return y

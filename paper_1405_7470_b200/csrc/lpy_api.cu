@@ -385,3 +385,101 @@ lpy_status lpy_gemm_f32_host(int64_t M, int64_t N, int64_t K, const float *A, in
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ saxpy
+namespace {
+
+constexpr int64_t kMaxSpan = int64_t(1) << 62;
+
+// Validation shared by the device and host entry points (include/lpy.h).
+lpy_status validate_saxpy(int64_t n, const float *x, int64_t incx, const float *y, int64_t incy) {
+    if (n < 0 || incx < 1 || incy < 1) return LPY_ERR_INVALID_VALUE;
+    if (n == 0) return LPY_OK;
+    if ((n - 1) > (kMaxSpan - 1) / incx || (n - 1) > (kMaxSpan - 1) / incy) return LPY_ERR_INVALID_VALUE;
+    if (x == nullptr || y == nullptr) return LPY_ERR_NULL_POINTER;
+    if ((reinterpret_cast<uintptr_t>(x) & 3) || (reinterpret_cast<uintptr_t>(y) & 3)) return LPY_ERR_MISALIGNED;
+    if (x == y && incx == incy) return LPY_OK;  // the same vector: y := alpha*y + y
+    const uintptr_t x0 = reinterpret_cast<uintptr_t>(x), x1 = x0 + uintptr_t((n - 1) * incx + 1) * 4;
+    const uintptr_t y0 = reinterpret_cast<uintptr_t>(y), y1 = y0 + uintptr_t((n - 1) * incy + 1) * 4;
+    if (x0 < y1 && y0 < x1) return LPY_ERR_ALIAS;
+    return LPY_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lpy_status lpy_saxpy_f32(int64_t n, float alpha, const float *x, int64_t incx, float *y, int64_t incy,
+                         void *stream) {
+    lpy_status st = validate_saxpy(n, x, incx, y, incy);
+    if (st != LPY_OK || n == 0) return st;
+    DeviceInfo dev;
+    if ((st = device_info(dev)) != LPY_OK) return st;
+    cudaError_t e = lpy::launch_saxpy(n, alpha, x, incx, y, incy, dev.sms, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? LPY_OK : cuda_fail(e);
+}
+
+lpy_status lpy_saxpy_f32_host(int64_t n, float alpha, const float *x, int64_t incx, float *y, int64_t incy,
+                              void *stream) {
+    lpy_status st = validate_saxpy(n, x, incx, y, incy);
+    if (st != LPY_OK || n == 0) return st;
+    DeviceInfo dev;
+    if ((st = device_info(dev)) != LPY_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool same = (x == y && incx == incy);
+    // Packed device copies (a strided host vector is gathered by a 2-D copy of
+    // 4-byte rows), in chunks pipelined over two internal streams: the upload
+    // of chunk c+1 overlaps chunk c's kernel and download (PCIe is full duplex).
+    float *dx = nullptr, *dy = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (!same) e = cudaMallocAsync(reinterpret_cast<void **>(&dx), size_t(n) * 4, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void **>(&dy), size_t(n) * 4, s);
+    const int64_t nchunk = n < (int64_t(1) << 20) ? 1 : 8;
+    const int64_t per = ((n + nchunk - 1) / nchunk + 3) / 4 * 4;
+    cudaStream_t su = nullptr, sd = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_done = nullptr, ev_up[8] = {}, ev_k[8] = {};
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&su, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
+    for (int c = 0; c < nchunk && e == cudaSuccess; ++c) {
+        e = cudaEventCreateWithFlags(&ev_up[c], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_k[c], cudaEventDisableTiming);
+    }
+    auto copy = [&](float *dst, int64_t dinc, const float *src, int64_t sinc, int64_t cnt, cudaMemcpyKind kind,
+                    cudaStream_t st_) {
+        if (dinc == 1 && sinc == 1) return cudaMemcpyAsync(dst, src, size_t(cnt) * 4, kind, st_);
+        return cudaMemcpy2DAsync(dst, size_t(dinc) * 4, src, size_t(sinc) * 4, 4, size_t(cnt), kind, st_);
+    };
+    if (e == cudaSuccess) e = cudaEventRecord(ev_fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(su, ev_fork, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, ev_fork, 0);
+    for (int64_t c = 0; c < nchunk && e == cudaSuccess; ++c) {
+        const int64_t i0 = c * per, cnt = std::min(n, i0 + per) - i0;
+        if (cnt <= 0) break;
+        if (!same) e = copy(dx + i0, 1, x + i0 * incx, incx, cnt, cudaMemcpyHostToDevice, su);
+        if (e == cudaSuccess) e = copy(dy + i0, 1, y + i0 * incy, incy, cnt, cudaMemcpyHostToDevice, su);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_up[c], su);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, ev_up[c], 0);
+        if (e == cudaSuccess)
+            e = lpy::launch_saxpy(cnt, alpha, same ? dy + i0 : dx + i0, 1, dy + i0, 1, dev.sms, sd);
+        if (e == cudaSuccess) e = copy(y + i0 * incy, incy, dy + i0, 1, cnt, cudaMemcpyDeviceToHost, sd);
+    }
+    for (cudaStream_t x_ : {su, sd})
+        if (x_ && ev_done && cudaEventRecord(ev_done, x_) == cudaSuccess) cudaStreamWaitEvent(s, ev_done, 0);
+    if (dx) cudaFreeAsync(dx, s);
+    if (dy) cudaFreeAsync(dy, s);
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = e2;
+    for (cudaStream_t x_ : {su, sd})
+        if (x_) cudaStreamDestroy(x_);
+    for (cudaEvent_t x_ : {ev_fork, ev_done})
+        if (x_) cudaEventDestroy(x_);
+    for (int c = 0; c < 8; ++c) {
+        if (ev_up[c]) cudaEventDestroy(ev_up[c]);
+        if (ev_k[c]) cudaEventDestroy(ev_k[c]);
+    }
+    return e == cudaSuccess ? LPY_OK : cuda_fail(e);
+}
+
+}  // extern "C"

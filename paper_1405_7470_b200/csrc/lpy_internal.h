@@ -40,6 +40,10 @@ cudaError_t launch_3xtf32(const Problem &p, const Knobs &k, cudaStream_t s);
 bool tf32_supported(const Problem &p);
 bool tf32_available();  // the 3xTF32 kernel is compiled in
 
+// y := alpha * x + y (saxpy.cu); n > 0 handled, n <= 0 is a no-op.
+cudaError_t launch_saxpy(int64_t n, float alpha, const float *x, int64_t incx, float *y, int64_t incy,
+                         int num_sms, cudaStream_t s);
+
 // dst[line*ld_dst + e] = src[line*ld_src + e] for line < lines, e < inner.
 cudaError_t launch_repack(const float *src, int64_t ld_src, float *dst, int64_t ld_dst,
                           int64_t lines, int64_t inner, cudaStream_t s);

@@ -26,13 +26,15 @@ import numpy as np
 __all__ = [
     "DISTS", "ROW_MAJOR", "COL_MAJOR", "MATRIX_A", "MATRIX_B",
     "splitmix64", "matrix", "store", "load_logical", "identity", "permutation",
-    "min_ld",
+    "min_ld", "VECTOR_X", "VECTOR_Y", "vector", "strided",
 ]
 
 ROW_MAJOR = 0
 COL_MAJOR = 1
 MATRIX_A = 0
 MATRIX_B = 1
+VECTOR_X = 2
+VECTOR_Y = 3
 DISTS = ("uniform", "uniform01", "int", "wide")
 
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
@@ -87,6 +89,25 @@ def matrix(rows: int, cols: int, seed: int = 0, matrix_id: int = 0, dist: str = 
         ridx = np.arange(row0 + r, row0 + r + rr, dtype=np.uint64)
         out[r:r + rr] = _to_dist(_hash_block(seed, matrix_id, ridx, cidx), dist)
     return out
+
+
+def vector(n: int, seed: int = 0, vector_id: int = VECTOR_X, dist: str = "uniform",
+           start: int = 0) -> np.ndarray:
+    """Logical fp32 vector of n elements; element i depends only on
+    (seed, vector_id, start + i) -- row 0 of a 1 x n matrix of the same
+    generator, so a rank or chunk can draw its slice alone."""
+    return matrix(1, n, seed=seed, matrix_id=vector_id, dist=dist, col0=start)[0]
+
+
+def strided(v: np.ndarray, inc: int, pad_value: float = float("nan")) -> np.ndarray:
+    """Lay vector v out with increment inc (element i at buf[i*inc]); the gaps
+    hold pad_value (NaN: a kernel that reads them poisons its result)."""
+    n = v.shape[0]
+    if n == 0:
+        return np.zeros(0, dtype=np.float32)
+    buf = np.full((n - 1) * inc + 1, pad_value, dtype=np.float32)
+    buf[::inc] = v
+    return buf
 
 
 def min_ld(rows: int, cols: int, layout: int) -> int:

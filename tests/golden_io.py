@@ -31,3 +31,23 @@ def read_golden(name):
     C = block("C", M)
     assert A.shape == (M, K) and B.shape == (K, N) and C.shape == (M, N)
     return M, N, K, A.astype(np.float32), B.astype(np.float32), C
+
+
+SAXPY_DIR = os.path.join(GOLDEN_DIR, "saxpy")
+
+
+def saxpy_golden_files():
+    return sorted(f for f in os.listdir(SAXPY_DIR) if f.endswith(".txt"))
+
+
+def read_saxpy_golden(name):
+    """(n, alpha, incx, incy, x buffer, y buffer, expected out[0:n])."""
+    lines = [ln.split("#", 1)[0].strip() for ln in open(os.path.join(SAXPY_DIR, name))]
+    lines = [ln for ln in lines if ln]
+    assert lines[0] == "n alpha incx incy"
+    n, alpha, incx, incy = lines[1].split()
+    assert lines[2] == "x" and lines[4] == "y" and lines[6] == "out"
+    x = np.array([float(v) for v in lines[3].split()], dtype=np.float32)
+    y = np.array([float(v) for v in lines[5].split()], dtype=np.float32)
+    out = np.array([float(v) for v in lines[7].split()])
+    return int(n), float(alpha), int(incx), int(incy), x, y, out

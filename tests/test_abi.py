@@ -28,7 +28,8 @@ def declared_functions():
 def test_header_declares_the_boundary():
     assert declared_functions() == sorted([
         "lpy_gemm_f32", "lpy_gemm_f32_ex", "lpy_gemm_f32_host", "lpy_select_path",
-        "lpy_status_string", "lpy_last_cuda_error", "lpy_version"])
+        "lpy_status_string", "lpy_last_cuda_error", "lpy_version", "lpy_saxpy_f32",
+        "lpy_saxpy_f32_host"])
 
 
 def test_library_exports_every_declared_symbol():
@@ -39,7 +40,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_version_and_status_strings():
-    assert lpy.lpy_version() == 1
+    assert lpy.lpy_version() == 2
     for code in range(10):
         s = lpy.lpy_status_string(code)
         assert s.startswith("LPY_")
@@ -119,3 +120,25 @@ def test_operand_layout_inference():
     y = torch.empty(5, 12)[:, :7]
     assert lpy.operand_layout(y) == (lpy.ROW_MAJOR, 12)
     assert lpy.operand_layout(torch.empty(6, 8)[::2, ::2]) is None
+
+
+def saxpy_call(n=4, alpha=1.0, x=FAKE, incx=1, y=FAKE + (1 << 20), incy=1, host=False):
+    fn = lpy.lpy_saxpy_f32_host if host else lpy.lpy_saxpy_f32
+    return fn(n, alpha, x, incx, y, incy, None)
+
+
+@pytest.mark.parametrize("host", [False, True])
+@pytest.mark.parametrize("kw,code", [
+    (dict(n=-1), 1), (dict(incx=0), 1), (dict(incy=-2), 1), (dict(n=1 << 40, incx=1 << 30), 1),
+    (dict(x=0), 3), (dict(y=0), 3),
+    (dict(x=FAKE + 2), 4), (dict(y=FAKE + (1 << 20) + 1), 4),
+    (dict(y=FAKE + 8), 5), (dict(y=FAKE, incy=2), 5), (dict(x=FAKE + (1 << 20) - 4), 5),
+    (dict(n=3, incx=4, y=FAKE + 4), 5),
+])
+def test_saxpy_validation_errors_precede_cuda(kw, code, host):
+    assert saxpy_call(host=host, **kw) == code
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_saxpy_empty_is_a_noop(host):
+    assert saxpy_call(n=0, x=0, y=0, host=host) == 0
