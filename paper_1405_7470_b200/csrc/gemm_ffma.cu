@@ -70,7 +70,19 @@ struct Params {
     int64_t ldc;
     int tiles_m, tiles_n, num_tiles, k_blocks, group;
     int c_vec;  // C base and ldc allow 16-byte stores
+    // split-K (bulk/edge specialisation for under-filled grids): work unit
+    // u = tile * splits + slice covers k-blocks [slice*KB/splits, (slice+1)*KB/splits)
+    int splits, num_units;
+    float *ws;       // [num_units][BM*BN] partial tiles (splits > 1)
+    int *sem;        // [num_tiles] arrival counters, zero on entry, left zero on exit
 };
+
+__device__ __forceinline__ void unit_range(int u, const Params &p, int &t, int &kb0, int &kb1) {
+    t = u / p.splits;
+    const int s = u - t * p.splits;
+    kb0 = int((int64_t(s) * p.k_blocks) / p.splits);
+    kb1 = int((int64_t(s + 1) * p.k_blocks) / p.splits);
+}
 
 // Packed fp32 pairs for FFMA2.  c += a * b with c, b packed (lo, hi) pairs and
 // the scalar a broadcast: fma.rn.f32x2 = two fp32 RN fused multiply-adds,
@@ -194,11 +206,12 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
                 tma_prefetch_desc(&tmB);
                 int stage = 0;
                 uint32_t phase = 0;
-                for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-                    int tm, tn;
+                for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+                    int t, kb0, kb1, tm, tn;
+                    unit_range(u, p, t, kb0, kb1);
                     tile_coords(t, p, tm, tn);
                     const int m0 = tm * BM, n0 = tn * BN;
-                    for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait_sleep(&empty[stage], phase ^ 1, 2000);
                         mbar_arrive_expect_tx(&full[stage], G::TMA_BYTES);
                         if constexpr (AK) tma_load_2d(raw_a(stage), &tmA, &full[stage], kb * BK, m0);
@@ -214,8 +227,10 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
             const int xw = warp - CWARPS - 1;
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-                for (int kb = 0; kb < p.k_blocks; ++kb) {
+            for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+                int t, kb0, kb1;
+                unit_range(u, p, t, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     if constexpr (G::XA) transpose_tile(raw_a(stage), x_a(stage), xw, lane);
                     if constexpr (G::XB) transpose_tile(raw_b(stage), x_b(stage), xw, lane);
@@ -235,8 +250,10 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
     const int lm = lane >> 2, ln = lane & 3;
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        int tm, tn;
+    __shared__ int last_flag;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+        int t, kb0, kb1, tm, tn;
+        unit_range(u, p, t, kb0, kb1);
         tile_coords(t, p, tm, tn);
         // acc2[i][jp] = (acc(i, 2jp), acc(i, 2jp+1)): pairs along n, where one
         // LDS.128 of the MN-major B tile delivers adjacent columns
@@ -246,7 +263,7 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
 
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
             if constexpr (!(G::XA && G::XB)) mbar_wait(&full[stage], phase);   // reads a raw tile
             if constexpr (G::X) mbar_wait(&xfull[stage], phase);
             const float *sa = G::XA ? x_a(stage) : raw_a(stage);
@@ -270,6 +287,45 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+
+        if (p.splits > 1) {
+            // ---------------------------------------- split-K fix-up
+            // Every slice parks its partial tile in the workspace (each thread its
+            // own 64 floats, contiguous); the slice that arrives last sums all
+            // partials in slice order -- a fixed order, so the result does not
+            // depend on which slice finishes first -- and stores C.
+            const int ctid = threadIdx.x;   // 0 .. CWARPS*32-1
+            float4 *mine = reinterpret_cast<float4 *>(p.ws + int64_t(u) * (BM * BN)) + ctid * 16;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                float lo0, hi0, lo1, hi1, lo2, hi2, lo3, hi3;
+                unpack2(acc2[i][0], lo0, hi0); unpack2(acc2[i][1], lo1, hi1);
+                unpack2(acc2[i][2], lo2, hi2); unpack2(acc2[i][3], lo3, hi3);
+                __stcg(mine + 2 * i, make_float4(lo0, hi0, lo1, hi1));
+                __stcg(mine + 2 * i + 1, make_float4(lo2, hi2, lo3, hi3));
+            }
+            __threadfence();
+            named_bar_sync(1, CWARPS * 32);
+            if (ctid == 0) last_flag = (atomicAdd(p.sem + t, 1) == p.splits - 1);
+            named_bar_sync(1, CWARPS * 32);
+            const bool last = last_flag;
+            if (!last) continue;
+            __threadfence();
+            const float4 *base = reinterpret_cast<const float4 *>(p.ws + int64_t(t) * p.splits * (BM * BN)) + ctid * 16;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                float4 s0 = __ldcg(base + 2 * i), s1 = __ldcg(base + 2 * i + 1);
+                for (int sl = 1; sl < p.splits; ++sl) {
+                    const float4 q0 = __ldcg(base + sl * (BM * BN / 4) + 2 * i);
+                    const float4 q1 = __ldcg(base + sl * (BM * BN / 4) + 2 * i + 1);
+                    s0.x += q0.x; s0.y += q0.y; s0.z += q0.z; s0.w += q0.w;
+                    s1.x += q1.x; s1.y += q1.y; s1.z += q1.z; s1.w += q1.w;
+                }
+                acc2[i][0] = pack2(s0.x, s0.y); acc2[i][1] = pack2(s0.z, s0.w);
+                acc2[i][2] = pack2(s1.x, s1.y); acc2[i][3] = pack2(s1.z, s1.w);
+            }
+            if (ctid == 0) p.sem[t] = 0;   // ready for the next launch
         }
 
         // ------------------------------------------------ epilogue (ragged-edge stores)
@@ -298,6 +354,23 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
     }
 }
 
+// Split-K factor for an under-filled grid (the paper's separate code for edge
+// cases, read as "bulk tiles vs the ragged last wave"): the S in
+// 1..8 whose (tile, slice) units fill the persistent grid's waves best, keeping
+// at least 4 k-blocks per slice; S = 1 unless it gains more than 10%.
+int choose_splits(int tiles, int k_blocks, int num_sms) {
+    auto eff = [&](int s) {
+        const int64_t units = int64_t(tiles) * s;
+        const int64_t waves = (units + num_sms - 1) / num_sms;
+        return double(units) / double(waves * num_sms);
+    };
+    int best = 1;
+    double best_eff = eff(1);
+    for (int s = 2; s <= 8 && k_blocks / s >= 4; ++s)
+        if (eff(s) > best_eff * 1.10 + 1e-9) { best = s; best_eff = eff(s); }
+    return best;
+}
+
 template <bool AK, bool BKM>
 static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     using G = Geo<AK, BKM>;
@@ -319,9 +392,26 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     prm.k_blocks = (p.K + BK - 1) / BK;
     prm.group = kn.raster_group > 0 ? kn.raster_group : 16;
     prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
+    prm.splits = choose_splits(prm.num_tiles, prm.k_blocks, kn.num_sms);
+    prm.num_units = prm.num_tiles * prm.splits;
+    prm.ws = nullptr;
+    prm.sem = nullptr;
     int grid = kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms;
-    if (grid > prm.num_tiles) grid = prm.num_tiles;
+    if (grid > prm.num_units) grid = prm.num_units;
     if (grid < 1) grid = 1;
+    if (prm.splits > 1) {
+        // The split is fixed by the shape and the device's SM count (never by
+        // opts.num_ctas), so results stay bitwise grid-invariant.  Scratch is
+        // stream-ordered: partial tiles, then the zeroed arrival counters.
+        const size_t ws_bytes = size_t(prm.num_units) * BM * BN * 4;
+        char *buf = nullptr;
+        e = cudaMallocAsync(reinterpret_cast<void **>(&buf), ws_bytes + size_t(prm.num_tiles) * 4, s);
+        if (e != cudaSuccess) return e;
+        prm.ws = reinterpret_cast<float *>(buf);
+        prm.sem = reinterpret_cast<int *>(buf + ws_bytes);
+        e = cudaMemsetAsync(prm.sem, 0, size_t(prm.num_tiles) * 4, s);
+        if (e != cudaSuccess) { cudaFreeAsync(buf, s); return e; }
+    }
 
     auto kern = gemm_ffma_kernel<AK, BKM>;
     static bool attr_done = false;  // benign race: setting the attribute twice is harmless
@@ -331,7 +421,9 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
         attr_done = true;
     }
     kern<<<grid, G::THREADS, G::SMEM_BYTES, s>>>(ta, tb, prm);
-    return cudaGetLastError();
+    e = cudaGetLastError();
+    if (prm.ws) cudaFreeAsync(prm.ws, s);
+    return e;
 }
 
 }  // namespace ffma

@@ -299,3 +299,24 @@ extern "C" int lpy_probe_umma_rate_fmt(int N, int fa, int fb, int iters, int cta
                          int(smem));
     return int(cudaLaunchKernelEx(&cfg, lpy::probe::umma_rate_fmt_kernel<1>, N, fa, fb, iters, cycles_dev));
 }
+
+// ---------------------------------------------------------------- launch overhead
+// An empty kernel with `threads` threads and `smem` bytes of dynamic shared
+// memory (touching one word so it is really allocated): how much fixed cost a
+// launch with the GEMM kernels' resource shape carries.
+namespace lpy {
+namespace probe {
+__global__ void empty_smem_kernel(int *out) {
+    extern __shared__ int sm[];
+    if (threadIdx.x == 0) sm[0] = blockIdx.x;
+    __syncthreads();
+    if (threadIdx.x == 0 && sm[0] == -1) out[0] = 1;
+}
+}  // namespace probe
+}  // namespace lpy
+
+extern "C" int lpy_probe_empty_launch(int ctas, int threads, int smem, int *out, void *stream) {
+    cudaFuncSetAttribute(lpy::probe::empty_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    lpy::probe::empty_smem_kernel<<<ctas, threads, smem, static_cast<cudaStream_t>(stream)>>>(out);
+    return int(cudaGetLastError());
+}

@@ -8,26 +8,30 @@
 
 namespace lpy {
 
-__global__ void repack_kernel(const float *__restrict__ src, int64_t ld_src, float *__restrict__ dst,
-                              int64_t ld_dst, int64_t lines, int64_t inner) {
-    for (int64_t line = blockIdx.y; line < lines; line += gridDim.y) {
+// One warp per line (grid-stride over lines): 32 consecutive 4-byte loads and
+// stores per instruction, so even short lines (the ragged config's 777 floats)
+// move at full coalescing; the grid fills every SM once.
+__global__ void __launch_bounds__(256) repack_kernel(const float *__restrict__ src, int64_t ld_src,
+                                                     float *__restrict__ dst, int64_t ld_dst, int64_t lines,
+                                                     int64_t inner) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t line = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); line < lines;
+         line += warps) {
         const float *s = src + line * ld_src;
         float *d = dst + line * ld_dst;
-        for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < ld_dst;
-             e += int64_t(gridDim.x) * blockDim.x)
-            d[e] = e < inner ? s[e] : 0.f;   // pad the tail of each line with zeros
+        for (int64_t e = lane; e < ld_dst; e += 32) d[e] = e < inner ? s[e] : 0.f;   // zero the pad
     }
 }
 
 cudaError_t launch_repack(const float *src, int64_t ld_src, float *dst, int64_t ld_dst, int64_t lines,
                           int64_t inner, cudaStream_t s) {
     if (lines <= 0 || inner <= 0) return cudaSuccess;
-    const int threads = 256;
-    int64_t gx = (ld_dst + threads - 1) / threads;
-    if (gx > 64) gx = 64;
-    int64_t gy = lines < 65535 ? lines : 65535;
-    repack_kernel<<<dim3(unsigned(gx), unsigned(gy)), threads, 0, s>>>(src, ld_src, dst, ld_dst, lines,
-                                                                       inner);
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t blocks = (lines + 7) / 8;
+    if (blocks > int64_t(sms) * 8) blocks = int64_t(sms) * 8;
+    repack_kernel<<<unsigned(blocks), 256, 0, s>>>(src, ld_src, dst, ld_dst, lines, inner);
     return cudaGetLastError();
 }
 
