@@ -36,6 +36,9 @@ cudaError_t make_tmap_2d(CUtensorMap *tm, const float *base, uint64_t inner, uin
                          uint64_t ld, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swizzle);
 
 cudaError_t launch_ffma(const Problem &p, const Knobs &k, cudaStream_t s);
+// split-K slices for `tiles` output tiles of `k_blocks` k-blocks on `workers`
+// persistent CTAs (pairs); >= min_kb k-blocks per slice (gemm_ffma.cu)
+int choose_splits(int tiles, int k_blocks, int workers, int min_kb);
 cudaError_t launch_3xtf32(const Problem &p, const Knobs &k, cudaStream_t s);
 bool tf32_supported(const Problem &p);
 bool tf32_available();  // the 3xTF32 kernel is compiled in
