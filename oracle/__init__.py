@@ -50,6 +50,8 @@ def _load():
             lib.lpy_oracle_gemm_elems_f64.restype = i32
             lib.lpy_oracle_saxpy_f64.argtypes = [i64, ctypes.c_float, fp, i64, fp, i64, dp, i32]
             lib.lpy_oracle_saxpy_f64.restype = i32
+            lib.lpy_oracle_coulomb_f64.argtypes = [i64, fp, i64, i64, fp, i64, fp, dp, dp, i32]
+            lib.lpy_oracle_coulomb_f64.restype = i32
             lib.lpy_oracle_max_threads.argtypes = []
             lib.lpy_oracle_max_threads.restype = i32
             _lib = lib
@@ -132,6 +134,25 @@ def saxpy_error_ulps(y32, ref64):
     r = np.abs(y - ref) / (half + np.ldexp(mag, -52))
     r = np.where(np.isnan(y), np.inf, r)
     return float(r.max())
+
+
+def coulomb(nt, targets, ldt, ns, sources, lds, q, nthreads=0):
+    """float64 potentials phi[i] = sum_{j: r_ij != 0} q_j / r_ij and the parity
+    normaliser D[i] = sum_j |q_j| / r_ij (Table 1's 3D Coulomb row).
+    targets / sources: flat float32 buffers, point i at [i*ld : i*ld+3]."""
+    for b in (targets, sources, q):
+        _check_buf(b)
+    if nt > 0 and targets.size < (nt - 1) * ldt + 3:
+        raise ValueError("targets buffer too short")
+    if ns > 0 and (sources.size < (ns - 1) * lds + 3 or q.size < ns):
+        raise ValueError("sources / charges buffer too short")
+    phi = np.empty(max(nt, 0), dtype=np.float64)
+    D = np.empty(max(nt, 0), dtype=np.float64)
+    rc = _load().lpy_oracle_coulomb_f64(nt, _ptr(targets), ldt, ns, _ptr(sources), lds, _ptr(q),
+                                         _ptr(phi), _ptr(D), int(nthreads))
+    if rc != 0:
+        raise ValueError("oracle rejected its arguments")
+    return phi, D
 
 
 def max_threads() -> int:

@@ -8,7 +8,8 @@
  * and this file shares no code, header, table or helper with the CUDA side.
  *
  * What it computes (section 2.1, the reduction example;
- * and, at the end of this file, Table 1's saxpy):
+ * and, at the end of this file, Table 1's saxpy, and 3D Coulomb
+ * potential):
  *
  *     c[i,j] = sum(k, a[i,k]*b[k,j])
  *
@@ -147,6 +148,50 @@ int lpy_oracle_saxpy_f64(int64_t n, float alpha, const float *x, int64_t incx,
 #endif
     for (int64_t i = 0; i < n; ++i)
         out[i] = (double)alpha * (double)x[i * incx] + (double)y[i * incy];
+    (void)nthreads;
+    return 0;
+}
+
+/* ------------------------------------------------------------------ Coulomb
+ * Table 1's "3D Coulomb pot." row (section 3): the potential
+ * at each target of a set of point charges,
+ *
+ *     phi[i] = sum_{j : r_ij != 0} q[j] / r_ij,
+ *     r_ij   = sqrt((tx_i - sx_j)^2 + (ty_i - sy_j)^2 + (tz_i - sz_j)^2),
+ *
+ * for i < nt over the sources j < ns, j ascending.  A source at exactly the
+ * target's position (r_ij = 0: the target itself when targets == sources)
+ * contributes nothing (reading C1).  Target i's coordinates are
+ * t[i*ldt + 0..2], source j's s[j*lds + 0..2], its charge q[j] (fp32 in).
+ * Everything is float64: coordinate differences of fp32 values are exact in
+ * float64, the rest rounds at 2^-53 per operation, so phi is exact to far
+ * below the GPU tolerance.  Also returns D[i] = sum_j |q[j]| / r_ij, the
+ * normaliser of the parity metric |phi - phi_ref| / D.  Parallel over i only;
+ * returns 0, or -1 on bad arguments. */
+int lpy_oracle_coulomb_f64(int64_t nt, const float *t, int64_t ldt,
+                           int64_t ns, const float *s, int64_t lds, const float *q,
+                           double *phi, double *D, int nthreads)
+{
+    if (nt < 0 || ns < 0 || ldt < 3 || lds < 3) return -1;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 64) num_threads(nthreads)
+#endif
+    for (int64_t i = 0; i < nt; ++i) {
+        const double x = t[i * ldt], y = t[i * ldt + 1], z = t[i * ldt + 2];
+        double acc = 0.0, dacc = 0.0;
+        for (int64_t j = 0; j < ns; ++j) {
+            const double dx = x - (double)s[j * lds];
+            const double dy = y - (double)s[j * lds + 1];
+            const double dz = z - (double)s[j * lds + 2];
+            const double r = sqrt(dx * dx + dy * dy + dz * dz);
+            if (r == 0.0) continue;          /* coincident: excluded (reading C1) */
+            acc += (double)q[j] / r;
+            dacc += fabs((double)q[j]) / r;
+        }
+        phi[i] = acc;
+        if (D) D[i] = dacc;
+    }
     (void)nthreads;
     return 0;
 }

@@ -26,7 +26,7 @@ import numpy as np
 __all__ = [
     "DISTS", "ROW_MAJOR", "COL_MAJOR", "MATRIX_A", "MATRIX_B",
     "splitmix64", "matrix", "store", "load_logical", "identity", "permutation",
-    "min_ld", "VECTOR_X", "VECTOR_Y", "vector", "strided",
+    "min_ld", "VECTOR_X", "VECTOR_Y", "vector", "strided", "PARTICLES", "CHARGES", "particles",
 ]
 
 ROW_MAJOR = 0
@@ -35,6 +35,8 @@ MATRIX_A = 0
 MATRIX_B = 1
 VECTOR_X = 2
 VECTOR_Y = 3
+PARTICLES = 4
+CHARGES = 5
 DISTS = ("uniform", "uniform01", "int", "wide")
 
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
@@ -108,6 +110,22 @@ def strided(v: np.ndarray, inc: int, pad_value: float = float("nan")) -> np.ndar
     buf = np.full((n - 1) * inc + 1, pad_value, dtype=np.float32)
     buf[::inc] = v
     return buf
+
+
+def particles(n: int, seed: int = 0, charges: str = "uniform", start: int = 0,
+              ld: int = 3) -> tuple[np.ndarray, np.ndarray]:
+    """n point charges for the 3D Coulomb row:
+    positions uniform in the unit cube [0, 1)^3 on a 2^-23 grid (so every
+    coordinate difference is exact in fp32 and float64), charges from
+    `charges` ("uniform": [-1, 1), "uniform01": [0, 1), "int": [-8, 8]).
+    Returns (flat positions buffer, point i at [i*ld : i*ld+3]; charges)."""
+    pos = matrix(n, 3, seed=seed, matrix_id=PARTICLES, dist="uniform01", row0=start)
+    q = vector(n, seed=seed, vector_id=CHARGES, dist=charges, start=start)
+    if ld == 3:
+        return np.ascontiguousarray(pos).reshape(-1), q
+    buf = np.full((n, ld), np.nan, dtype=np.float32)
+    buf[:, :3] = pos
+    return buf.reshape(-1)[: max(0, (n - 1) * ld + 3)].copy(), q
 
 
 def min_ld(rows: int, cols: int, layout: int) -> int:

@@ -51,3 +51,23 @@ def read_saxpy_golden(name):
     y = np.array([float(v) for v in lines[5].split()], dtype=np.float32)
     out = np.array([float(v) for v in lines[7].split()])
     return int(n), float(alpha), int(incx), int(incy), x, y, out
+
+
+COULOMB_DIR = os.path.join(GOLDEN_DIR, "coulomb")
+
+
+def coulomb_golden_files():
+    return sorted(f for f in os.listdir(COULOMB_DIR) if f.endswith(".txt"))
+
+
+def read_coulomb_golden(name):
+    """(sources (ns,3) f32, charges (ns,) f32, targets (nt,3) f32, expected phi (nt,))."""
+    lines = [ln.split("#", 1)[0].strip() for ln in open(os.path.join(COULOMB_DIR, name))]
+    lines = [ln for ln in lines if ln]
+    i_t, i_p = lines.index("targets x y z"), lines.index("phi")
+    assert lines[0] == "sources x y z q"
+    src = np.array([[float(v) for v in ln.split()] for ln in lines[1:i_t]])
+    tgt = np.array([[float(v) for v in ln.split()] for ln in lines[i_t + 1:i_p]])
+    phi = np.array([float(ln) for ln in lines[i_p + 1:]])
+    assert src.shape[1] == 4 and tgt.shape[1] == 3 and phi.shape[0] == tgt.shape[0]
+    return (src[:, :3].astype(np.float32), src[:, 3].astype(np.float32), tgt.astype(np.float32), phi)
