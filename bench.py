@@ -432,6 +432,63 @@ def time_saxpy(args, device):
             "data": "synthetic: torch.rand seeded 0, uniform[-1,1), alpha = 1.5"}
 
 
+def time_coulomb(args, device):
+    """Table 1's 3D Coulomb potential row: the self-potential
+    of N = 2^16 synthetic point charges (unit cube, charges uniform[-1,1)),
+    targets == sources, through lpy_coulomb_f32; pairs/s = N^2 / kernel time
+    (the loop domain {[i, j]}, self pairs included in the count)."""
+    import numpy as np
+    import torch
+    import oracle
+    import paper_1405_7470_b200 as lpy
+    import synth
+    n = args.coulomb_n
+    pos, q = synth.particles(n, seed=0)
+    P = torch.from_numpy(pos.reshape(n, 3)).to(device)
+    Q = torch.from_numpy(q).to(device)
+    phi = torch.empty(n, device=device)
+    lpy.coulomb(P, P, Q, out=phi)
+    torch.cuda.synchronize()
+    idx = np.random.default_rng(0).choice(n, 256, replace=False)
+    tsel = np.ascontiguousarray(pos.reshape(n, 3)[idx]).reshape(-1)
+    t0 = time.perf_counter()
+    ref, D = oracle.coulomb(idx.size, tsel, 3, n, pos, 3, q)
+    cpu_dt = time.perf_counter() - t0
+    err = float(np.max(np.abs(phi.cpu().numpy()[idx].astype(np.float64) - ref) / D))
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        lpy.coulomb(P, P, Q, out=phi)
+    torch.cuda.synchronize()
+    per = []
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            lpy.coulomb(P, P, Q, out=phi)
+            e1.record(stream)
+            per.append((e0, e1))
+        torch.cuda.synchronize()
+    ms = statistics.mean(a.elapsed_time(b) for a, b in per)
+    pairs = float(n) * n
+    peaks, src = load_peaks()
+    mhz = peaks.get("sm_max_mhz", 1965.0)
+    peak = 148 * 16 * mhz * 1e6       # MUFU.RSQ: 16 per clock per SM, one per pair
+    achieved = pairs / (ms * 1e-3)
+    return {"metric": "3D Coulomb potential pairs/s (self-potential, N^2 pairs per call)",
+            "value": round(achieved / 1e6, 1), "unit": "M pairs/s", "n": n, "ms_per_call": round(ms, 4),
+            "calls": args.steps, "gpu_launches": 3 * args.steps,
+            "roofline": {"bound": "alu", "achieved": round(achieved / 1e12, 4), "peak": round(peak / 1e12, 4),
+                         "unit": "T pairs/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "algorithmic_bytes": 16 * n + 16 * n,
+                         "peak_note": f"MUFU.RSQ bound: 148 SM x 16/clk x {mhz} MHz ({src} clock), one rsqrt per pair"},
+            "parity_sampled_max_norm_err": err,
+            "cpu_baseline": {"value": round(idx.size * float(n) / cpu_dt / 1e6, 1), "unit": "M pairs/s",
+                             "cores": oracle.max_threads(), "kind": "oracle",
+                             "sample": f"{idx.size} targets x {n} sources, float64"},
+            "clocks": clk.summary(),
+            "data": "synthetic: SplitMix64 positions uniform in [0,1)^3 (2^-23 grid), charges uniform[-1,1)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -451,6 +508,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--saxpy-n", type=int, default=1 << 28, help="saxpy length (0 = skip the saxpy line)")
+    ap.add_argument("--coulomb-n", type=int, default=1 << 16, help="Coulomb particles (0 = skip)")
     args = ap.parse_args()
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
 
@@ -486,6 +544,7 @@ def main():
         also = time_path(args, args.also, rank, world, device, dist_on)
     e2e = None if args.no_e2e else time_e2e(args, main_path, rank, world, device)
     sax = time_saxpy(args, device) if (args.saxpy_n > 0 and rank == 0 and not dist_on) else None
+    coul = time_coulomb(args, device) if (args.coulomb_n > 0 and rank == 0 and not dist_on) else None
 
     if rank == 0:
         n = args.n
@@ -532,6 +591,8 @@ def main():
             line["multi_gpu"] = res["multi"]
         if sax is not None:
             line["saxpy"] = sax
+        if coul is not None:
+            line["coulomb"] = coul
         if also is not None:
             ams = also["total_ms"] / args.steps
             line["alt_path"] = {"path": also["path"], "value": round(flops / (ams * 1e-3) / 1e9, 1),

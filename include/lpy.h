@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define LPY_VERSION 2
+#define LPY_VERSION 3
 
 typedef enum { LPY_ROW_MAJOR = 0, LPY_COL_MAJOR = 1 } lpy_layout;
 
@@ -146,6 +146,36 @@ lpy_status lpy_saxpy_f32(int64_t n, float alpha, const float *x, int64_t incx, f
  * bandwidth). */
 lpy_status lpy_saxpy_f32_host(int64_t n, float alpha, const float *x, int64_t incx, float *y,
                               int64_t incy, void *stream);
+
+/* ---------------------------------------------------------------- Coulomb
+ * phi[i] := sum_{j : r_ij != 0} q[j] / r_ij for i < nt: the 3D Coulomb
+ * potential of ns point charges at nt targets, Table 1's third workload
+ * (section 3), reported in pairs/s (nt * ns per call).
+ *   targets: t[i*ldt + 0..2] = (x, y, z) of target i, ldt >= 3 (ELEMENTS);
+ *   sources: s[j*lds + 0..2] = (x, y, z) of source j, lds >= 3; q[j] its charge;
+ *   phi:     nt floats, OVERWRITTEN (ns == 0 gives zeros).
+ * r_ij = |t_i - s_j|.  A source exactly at a target (r_ij == 0, e.g. the
+ * target itself when the two sets are the same array) contributes nothing
+ * (reading C1).  fp32 in, fp32 out; accuracy (reading C2):
+ *     |phi_i - phi_exact_i| <= 5e-6 * sum_j |q_j| / r_ij
+ * for finite inputs whose nonzero coordinate differences have squares in the
+ * fp32 normal range (|d| in [2^-63, 2^63]).  Deterministic (fixed summation
+ * order for a given shape and device).  Device memory of the current device,
+ * owned by the caller; internal scratch (packed sources, slice partials) is
+ * stream-ordered on `stream`.  phi must not overlap t, s or q
+ * (LPY_ERR_ALIAS).  nt == 0 is a no-op.  Errors as for lpy_gemm_f32:
+ * LPY_ERR_INVALID_VALUE (nt/ns < 0), LPY_ERR_INVALID_LD (ldt/lds < 3),
+ * LPY_ERR_NULL_POINTER, LPY_ERR_MISALIGNED, LPY_ERR_ALIAS,
+ * LPY_ERR_UNSUPPORTED_DEVICE, LPY_ERR_OUT_OF_MEMORY, LPY_ERR_CUDA. */
+lpy_status lpy_coulomb_f32(int64_t nt, const float *t, int64_t ldt,
+                           int64_t ns, const float *s, int64_t lds, const float *q,
+                           float *phi, void *stream);
+
+/* End-to-end Coulomb on HOST buffers: uploads targets, sources and charges,
+ * runs lpy_coulomb_f32, downloads phi and SYNCHRONISES `stream`. */
+lpy_status lpy_coulomb_f32_host(int64_t nt, const float *t, int64_t ldt,
+                                int64_t ns, const float *s, int64_t lds, const float *q,
+                                float *phi, void *stream);
 
 /* Host-only: the path `requested` resolves to for this problem shape (no CUDA
  * calls).  Returns LPY_ERR_INVALID_VALUE for bad enum/sizes. */

@@ -25,7 +25,7 @@ __all__ = [
     "GemmOpts", "library_path", "load_library", "lpy_gemm_f32", "lpy_gemm_f32_ex",
     "lpy_gemm_f32_host", "lpy_select_path", "lpy_status_string", "lpy_last_cuda_error",
     "lpy_version", "gemm", "operand_layout", "gemm_host", "lpy_saxpy_f32", "lpy_saxpy_f32_host",
-    "saxpy", "saxpy_host",
+    "saxpy", "saxpy_host", "lpy_coulomb_f32", "lpy_coulomb_f32_host", "coulomb", "coulomb_host",
 ]
 
 ROW_MAJOR = 0
@@ -88,6 +88,11 @@ def load_library():
         lib.lpy_saxpy_f32.restype = i32
         lib.lpy_saxpy_f32_host.argtypes = saxpy_args
         lib.lpy_saxpy_f32_host.restype = i32
+        coul_args = [i64, vp, i64, i64, vp, i64, vp, vp, vp]
+        lib.lpy_coulomb_f32.argtypes = coul_args
+        lib.lpy_coulomb_f32.restype = i32
+        lib.lpy_coulomb_f32_host.argtypes = coul_args
+        lib.lpy_coulomb_f32_host.restype = i32
         lib.lpy_version.argtypes = []
         lib.lpy_version.restype = i32
         _lib = lib
@@ -125,6 +130,14 @@ def lpy_saxpy_f32(n, alpha, x, incx, y, incy, stream=None) -> int:
 
 def lpy_saxpy_f32_host(n, alpha, x, incx, y, incy, stream=None) -> int:
     return load_library().lpy_saxpy_f32_host(n, alpha, x, incx, y, incy, stream)
+
+
+def lpy_coulomb_f32(nt, t, ldt, ns, s, lds, q, phi, stream=None) -> int:
+    return load_library().lpy_coulomb_f32(nt, t, ldt, ns, s, lds, q, phi, stream)
+
+
+def lpy_coulomb_f32_host(nt, t, ldt, ns, s, lds, q, phi, stream=None) -> int:
+    return load_library().lpy_coulomb_f32_host(nt, t, ldt, ns, s, lds, q, phi, stream)
 
 
 def lpy_status_string(status: int) -> str:
@@ -249,3 +262,41 @@ def saxpy_host(alpha, x, y, stream=None):
     if st != 0:
         raise LpyError(st, "lpy_saxpy_f32_host")
     return y
+
+
+def _points(p, name):
+    import torch
+    if p.dtype != torch.float32 or p.dim() != 2 or p.shape[1] < 3 or (p.shape[0] > 1 and p.stride(1) != 1):
+        raise TypeError(f"{name} must be an (n, >=3) fp32 tensor with unit column stride")
+    return p.stride(0) if p.shape[0] > 1 else max(3, p.shape[1])
+
+
+def coulomb(targets, sources, charges, out=None, stream=None):
+    """phi[i] = sum_{j: r_ij != 0} q_j / r_ij on CUDA tensors through
+    lpy_coulomb_f32 (Table 1's 3D Coulomb potential).
+    targets (nt, >=3), sources (ns, >=3): x, y, z in the first three columns;
+    charges (ns,) contiguous; returns phi (nt,)."""
+    import torch
+    ldt, lds = _points(targets, "targets"), _points(sources, "sources")
+    if charges.dtype != torch.float32 or charges.dim() != 1 or charges.shape[0] != sources.shape[0] or \
+            (charges.shape[0] > 1 and charges.stride(0) != 1):
+        raise TypeError("charges must be a contiguous (ns,) fp32 tensor")
+    nt = targets.shape[0]
+    if out is None:
+        out = torch.empty(nt, dtype=torch.float32, device=targets.device)
+    st = lpy_coulomb_f32(nt, targets.data_ptr(), ldt, sources.shape[0], sources.data_ptr(), lds,
+                         charges.data_ptr(), out.data_ptr(), _stream_handle(stream))
+    if st != 0:
+        raise LpyError(st, "lpy_coulomb_f32")
+    return out
+
+
+def coulomb_host(targets, sources, charges, out, stream=None):
+    """End-to-end Coulomb on host (CPU, ideally pinned) tensors; synchronises."""
+    ldt, lds = _points(targets, "targets"), _points(sources, "sources")
+    st = lpy_coulomb_f32_host(targets.shape[0], targets.data_ptr(), ldt, sources.shape[0], sources.data_ptr(),
+                              lds, charges.data_ptr(), out.data_ptr(),
+                              _stream_handle(stream) if stream is not None else None)
+    if st != 0:
+        raise LpyError(st, "lpy_coulomb_f32_host")
+    return out

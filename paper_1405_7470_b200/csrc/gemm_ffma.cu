@@ -375,7 +375,7 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     prm.k_blocks = (p.K + BK - 1) / BK;
     prm.group = kn.raster_group > 0 ? kn.raster_group : 16;
     prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
-    prm.splits = choose_splits(prm.num_tiles, prm.k_blocks, kn.num_sms, 4);
+    prm.splits = choose_splits(prm.num_tiles, prm.k_blocks, kn.num_sms, 4, 8);
     prm.num_units = prm.num_tiles * prm.splits;
     prm.ws = nullptr;
     prm.sem = nullptr;
@@ -413,9 +413,9 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
 
 // Split-K factor for an under-filled grid (the paper's separate code for edge
 // cases, read as "bulk tiles vs the ragged last wave"): the S in
-// 1..8 whose (tile, slice) units fill `workers` persistent CTAs (pairs) best,
+// 1..max_splits whose (tile, slice) units fill `workers` persistent CTAs best,
 // keeping at least `min_kb` k-blocks per slice; S = 1 unless it gains > 10%.
-int choose_splits(int tiles, int k_blocks, int workers, int min_kb) {
+int choose_splits(int tiles, int k_blocks, int workers, int min_kb, int max_splits) {
     auto eff = [&](int s) {
         const int64_t units = int64_t(tiles) * s;
         const int64_t waves = (units + workers - 1) / workers;
@@ -423,7 +423,7 @@ int choose_splits(int tiles, int k_blocks, int workers, int min_kb) {
     };
     int best = 1;
     double best_eff = eff(1);
-    for (int s = 2; s <= 8 && k_blocks / s >= min_kb; ++s)
+    for (int s = 2; s <= max_splits && k_blocks / s >= min_kb; ++s)
         if (eff(s) > best_eff * 1.10 + 1e-9) { best = s; best_eff = eff(s); }
     return best;
 }

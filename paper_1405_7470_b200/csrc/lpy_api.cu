@@ -483,3 +483,73 @@ lpy_status lpy_saxpy_f32_host(int64_t n, float alpha, const float *x, int64_t in
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ Coulomb
+namespace {
+
+lpy_status validate_coulomb(int64_t nt, const float *t, int64_t ldt, int64_t ns, const float *s, int64_t lds,
+                            const float *q, const float *phi) {
+    if (nt < 0 || ns < 0 || nt > kMaxSpan / 64 || ns > kMaxSpan / 64) return LPY_ERR_INVALID_VALUE;
+    if (ldt < 3 || lds < 3 || ldt > kMaxSpan / 64 || lds > kMaxSpan / 64) return LPY_ERR_INVALID_LD;
+    struct Span { const float *p; int64_t n; };
+    const Span spans[4] = {{t, nt > 0 ? (nt - 1) * ldt + 3 : 0}, {s, ns > 0 ? (ns - 1) * lds + 3 : 0},
+                           {q, ns}, {phi, nt}};
+    for (const Span &sp : spans) {
+        if (sp.n == 0) continue;
+        if (sp.p == nullptr) return LPY_ERR_NULL_POINTER;
+        if (reinterpret_cast<uintptr_t>(sp.p) & 3) return LPY_ERR_MISALIGNED;
+    }
+    if (nt > 0) {
+        const uintptr_t o0 = reinterpret_cast<uintptr_t>(phi), o1 = o0 + uintptr_t(nt) * 4;
+        for (int k = 0; k < 3; ++k) {
+            if (spans[k].n == 0) continue;
+            const uintptr_t a0 = reinterpret_cast<uintptr_t>(spans[k].p), a1 = a0 + uintptr_t(spans[k].n) * 4;
+            if (a0 < o1 && o0 < a1) return LPY_ERR_ALIAS;
+        }
+    }
+    return LPY_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lpy_status lpy_coulomb_f32(int64_t nt, const float *t, int64_t ldt, int64_t ns, const float *s, int64_t lds,
+                           const float *q, float *phi, void *stream) {
+    lpy_status st = validate_coulomb(nt, t, ldt, ns, s, lds, q, phi);
+    if (st != LPY_OK || nt == 0) return st;
+    DeviceInfo dev;
+    if ((st = device_info(dev)) != LPY_OK) return st;
+    cudaError_t e = lpy::launch_coulomb(nt, t, ldt, ns, s, lds, q, phi, dev.sms, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? LPY_OK : cuda_fail(e);
+}
+
+lpy_status lpy_coulomb_f32_host(int64_t nt, const float *t, int64_t ldt, int64_t ns, const float *s,
+                                int64_t lds, const float *q, float *phi, void *stream) {
+    lpy_status st = validate_coulomb(nt, t, ldt, ns, s, lds, q, phi);
+    if (st != LPY_OK || nt == 0) return st;
+    DeviceInfo dev;
+    if ((st = device_info(dev)) != LPY_OK) return st;
+    cudaStream_t sm = static_cast<cudaStream_t>(stream);
+    const size_t tb = size_t(nt > 0 ? (nt - 1) * ldt + 3 : 0) * 4, sb = size_t(ns > 0 ? (ns - 1) * lds + 3 : 0) * 4;
+    const size_t qb = size_t(ns) * 4, pb = size_t(nt) * 4;
+    char *buf = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&buf), tb + sb + qb + pb + 64, sm);
+    if (e != cudaSuccess) return cuda_fail(e);
+    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+    float *dt = reinterpret_cast<float *>(buf);
+    float *ds = reinterpret_cast<float *>(buf + al(tb));
+    float *dq = reinterpret_cast<float *>(buf + al(tb) + al(sb));
+    float *dp = reinterpret_cast<float *>(buf + al(tb) + al(sb) + al(qb));
+    if (tb) e = cudaMemcpyAsync(dt, t, tb, cudaMemcpyHostToDevice, sm);
+    if (e == cudaSuccess && sb) e = cudaMemcpyAsync(ds, s, sb, cudaMemcpyHostToDevice, sm);
+    if (e == cudaSuccess && qb) e = cudaMemcpyAsync(dq, q, qb, cudaMemcpyHostToDevice, sm);
+    if (e == cudaSuccess) e = lpy::launch_coulomb(nt, dt, ldt, ns, ds, lds, dq, dp, dev.sms, sm);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(phi, dp, pb, cudaMemcpyDeviceToHost, sm);
+    cudaFreeAsync(buf, sm);
+    cudaError_t e2 = cudaStreamSynchronize(sm);
+    if (e == cudaSuccess) e = e2;
+    return e == cudaSuccess ? LPY_OK : cuda_fail(e);
+}
+
+}  // extern "C"

@@ -37,8 +37,8 @@ cudaError_t make_tmap_2d(CUtensorMap *tm, const float *base, uint64_t inner, uin
 
 cudaError_t launch_ffma(const Problem &p, const Knobs &k, cudaStream_t s);
 // split-K slices for `tiles` output tiles of `k_blocks` k-blocks on `workers`
-// persistent CTAs (pairs); >= min_kb k-blocks per slice (gemm_ffma.cu)
-int choose_splits(int tiles, int k_blocks, int workers, int min_kb);
+// persistent CTAs (pairs); >= min_kb k-blocks per slice, <= max_splits (gemm_ffma.cu)
+int choose_splits(int tiles, int k_blocks, int workers, int min_kb, int max_splits);
 cudaError_t launch_3xtf32(const Problem &p, const Knobs &k, cudaStream_t s);
 bool tf32_supported(const Problem &p);
 bool tf32_available();  // the 3xTF32 kernel is compiled in
@@ -46,6 +46,10 @@ bool tf32_available();  // the 3xTF32 kernel is compiled in
 // y := alpha * x + y (saxpy.cu); n > 0 handled, n <= 0 is a no-op.
 cudaError_t launch_saxpy(int64_t n, float alpha, const float *x, int64_t incx, float *y, int64_t incy,
                          int num_sms, cudaStream_t s);
+
+// phi := Coulomb potential of (s, q) at t (coulomb.cu); nt <= 0 is a no-op.
+cudaError_t launch_coulomb(int64_t nt, const float *t, int64_t ldt, int64_t ns, const float *s, int64_t lds,
+                           const float *q, float *phi, int num_sms, cudaStream_t st);
 
 // dst[line*ld_dst + e] = src[line*ld_src + e] for line < lines, e < inner.
 cudaError_t launch_repack(const float *src, int64_t ld_src, float *dst, int64_t ld_dst,

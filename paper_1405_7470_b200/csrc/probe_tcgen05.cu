@@ -320,3 +320,43 @@ extern "C" int lpy_probe_empty_launch(int ctas, int threads, int smem, int *out,
     lpy::probe::empty_smem_kernel<<<ctas, threads, smem, static_cast<cudaStream_t>(stream)>>>(out);
     return int(cudaGetLastError());
 }
+
+// ---------------------------------------------------------------- MUFU.RSQ rate
+// 16 independent rsqrt.approx chains per thread (the Coulomb kernel's bound):
+// results per second over the grid = 16 * iters * blocks * threads / time.
+namespace lpy {
+namespace probe {
+__global__ void rsqrt_rate_kernel(float *out, int iters, float x) {
+    float a[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = x + threadIdx.x * 1e-3f + j;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) asm volatile("rsqrt.approx.ftz.f32 %0, %0;" : "+f"(a[j]));
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s += a[j];
+    if (s == 12345.678f) out[0] = s;
+}
+
+// Accuracy of rsqrt.approx.ftz.f32 on n inputs: out[i] = rsqrt(in[i]).
+__global__ void rsqrt_eval_kernel(const float *in, float *out, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        float r;
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(in[i]));
+        out[i] = r;
+    }
+}
+}  // namespace probe
+}  // namespace lpy
+
+extern "C" int lpy_probe_rsqrt_rate(float *out, int iters, int blocks, int threads, void *stream) {
+    lpy::probe::rsqrt_rate_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(out, iters, 1.5f);
+    return int(cudaGetLastError());
+}
+
+extern "C" int lpy_probe_rsqrt_eval(const float *in, float *out, int n, void *stream) {
+    lpy::probe::rsqrt_eval_kernel<<<592, 256, 0, static_cast<cudaStream_t>(stream)>>>(in, out, n);
+    return int(cudaGetLastError());
+}

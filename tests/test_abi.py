@@ -29,7 +29,7 @@ def test_header_declares_the_boundary():
     assert declared_functions() == sorted([
         "lpy_gemm_f32", "lpy_gemm_f32_ex", "lpy_gemm_f32_host", "lpy_select_path",
         "lpy_status_string", "lpy_last_cuda_error", "lpy_version", "lpy_saxpy_f32",
-        "lpy_saxpy_f32_host"])
+        "lpy_saxpy_f32_host", "lpy_coulomb_f32", "lpy_coulomb_f32_host"])
 
 
 def test_library_exports_every_declared_symbol():
@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_version_and_status_strings():
-    assert lpy.lpy_version() == 2
+    assert lpy.lpy_version() == 3
     for code in range(10):
         s = lpy.lpy_status_string(code)
         assert s.startswith("LPY_")
@@ -142,3 +142,25 @@ def test_saxpy_validation_errors_precede_cuda(kw, code, host):
 @pytest.mark.parametrize("host", [False, True])
 def test_saxpy_empty_is_a_noop(host):
     assert saxpy_call(n=0, x=0, y=0, host=host) == 0
+
+
+def coulomb_call(nt=4, t=FAKE, ldt=3, ns=4, s=FAKE + (1 << 20), lds=3, q=FAKE + (2 << 20),
+                 phi=FAKE + (3 << 20), host=False):
+    fn = lpy.lpy_coulomb_f32_host if host else lpy.lpy_coulomb_f32
+    return fn(nt, t, ldt, ns, s, lds, q, phi, None)
+
+
+@pytest.mark.parametrize("host", [False, True])
+@pytest.mark.parametrize("kw,code", [
+    (dict(nt=-1), 1), (dict(ns=-2), 1), (dict(ldt=2), 2), (dict(lds=0), 2),
+    (dict(t=0), 3), (dict(s=0), 3), (dict(q=0), 3), (dict(phi=0), 3),
+    (dict(t=FAKE + 2), 4), (dict(q=FAKE + (2 << 20) + 1), 4), (dict(phi=FAKE + (3 << 20) + 3), 4),
+    (dict(phi=FAKE + 4), 5), (dict(phi=FAKE + (1 << 20) + 40), 5), (dict(phi=FAKE + (2 << 20) - 4), 5),
+])
+def test_coulomb_validation_errors_precede_cuda(kw, code, host):
+    assert coulomb_call(host=host, **kw) == code
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_coulomb_empty_targets_is_a_noop(host):
+    assert coulomb_call(nt=0, t=0, phi=0, host=host) == 0

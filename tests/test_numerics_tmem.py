@@ -165,3 +165,44 @@ def test_mma_rate_per_operand_format(probe):
                     key = f"cycles_per_mma_cg{cg}_fa{fa}_fb{fb}" + ("_same" if same else "")
                     RESULTS[key] = cyc.item() / iters
     print({k: v for k, v in RESULTS.items() if k.startswith("cycles_per_mma_cg")})
+
+
+def test_rsqrt_rate(probe):
+    """MUFU.RSQ throughput (rsqrt.approx.ftz.f32), the Coulomb kernel's bound:
+    per-SM results per clock at the measured SM clock."""
+    probe.lpy_probe_rsqrt_rate.argtypes = [ctypes.c_void_p] + [ctypes.c_int] * 3 + [ctypes.c_void_p]
+    out = torch.zeros(1, device="cuda")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    iters, blocks, threads = 4000, sms * 4, 256
+    probe.lpy_probe_rsqrt_rate(out.data_ptr(), 100, blocks, threads, None)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    probe.lpy_probe_rsqrt_rate(out.data_ptr(), iters, blocks, threads, None)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    per_s = 16.0 * iters * blocks * threads / (ms * 1e-3)
+    RESULTS["rsqrt_per_s"] = per_s
+    RESULTS["rsqrt_per_clk_per_sm_at_1965MHz"] = per_s / sms / 1.965e9
+    print(RESULTS)
+    assert per_s > 0
+
+
+def test_rsqrt_accuracy(probe):
+    """Max relative error of rsqrt.approx.ftz.f32 over every fp32 mantissa in
+    [1, 4) (two binades cover all exponent parities), against float64: the
+    per-term error in DESIGN.md reading C2's bound."""
+    probe.lpy_probe_rsqrt_eval.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    bits = np.arange(0x3F800000, 0x40800000, dtype=np.uint32)
+    x = bits.view(np.float32)
+    dx = torch.from_numpy(x).cuda()
+    dy = torch.empty_like(dx)
+    assert probe.lpy_probe_rsqrt_eval(dx.data_ptr(), dy.data_ptr(), x.size, None) == 0
+    torch.cuda.synchronize()
+    y = dy.cpu().numpy().astype(np.float64)
+    rel = np.abs(y * np.sqrt(x.astype(np.float64)) - 1.0)
+    RESULTS["rsqrt_max_rel_err"] = float(rel.max())
+    RESULTS["rsqrt_max_rel_err_log2"] = float(np.log2(rel.max()))
+    print(RESULTS)
+    assert rel.max() < 2.0 ** -21
