@@ -43,17 +43,19 @@
 namespace lpy {
 namespace tf32 {
 
-constexpr int BM = 128, BN = 256, BK = 16;   // BM rows per CTA; BN columns per tile
+constexpr int BM = 128, BK = 16;             // BM rows per CTA (the tile's BN columns: template, 128/192/256)
 constexpr int THREADS = 512;                 // 16 warps = 4 warpgroups
 constexpr int XFORM_WARP0 = 4, XFORM_WARPS = 4;
 constexpr int EPI_WARP0 = 8, EPI_WARPS = 8;
 constexpr int REGS_CTRL = 56, REGS_XFORM = 72, REGS_EPI = 192;   // 128*56 + 128*72 + 256*192 = 65536
 constexpr uint32_t TMEM_COLS = 512;          // 2 partial buffers x 256 columns
 
-template <int CG>
+template <int CG, int BN>
 struct Cfg {
     static constexpr int BN_CTA = BN / CG;                       // B columns staged per CTA
-    static constexpr int STAGES = CG == 2 ? 7 : 4;
+    static constexpr int EC = BN / 2;                            // columns per promotion thread
+    static constexpr uint32_t STAGE_BYTES_ = 2 * (BM * BK * 4 + BN_CTA * BK * 4);
+    static constexpr int STAGES = CG == 2 ? int((227 * 1024 - 1024 - 256 - 64) / STAGE_BYTES_) : 4;
     static constexpr uint32_t A_BYTES = BM * BK * 4;             // 8 KB
     static constexpr uint32_t B_BYTES = BN_CTA * BK * 4;         // 16 KB / CG
     static constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;     // TMA transaction per stage
@@ -68,7 +70,28 @@ struct Params {
     int tiles_m, tiles_n, num_tiles, k_blocks, group, promote;
     int c_vec;
     long long *trace;   // diagnostics build only (-DLPY_TRACE): per-CTA cycle counters
+    // Tail split (the ragged last wave): tiles [0, full_tiles) are one work unit
+    // each; every later tile is split into `splits` k-slices, so the last wave
+    // of short units fills all CTA pairs.  Slice partials are parked in `ws` and
+    // the slice that finishes a tile last adds them in slice order.
+    int full_tiles, splits, num_units;
+    float *ws;          // [(num_units - full_tiles)][CG][BM x BN] partial tiles
+    int *sem;           // [(num_tiles - full_tiles)][CG] arrival counters, zero on entry and exit
 };
+
+// Work unit u -> tile t, k-block range [kb0, kb1), and (for a split unit) its
+// index among the split units (-1 for a whole tile).
+__device__ __forceinline__ void unit_range(int u, const Params &p, int &t, int &kb0, int &kb1, int &su) {
+    if (u < p.full_tiles) {
+        t = u; kb0 = 0; kb1 = p.k_blocks; su = -1;
+        return;
+    }
+    su = u - p.full_tiles;
+    const int v = su / p.splits, sl = su - v * p.splits;
+    t = p.full_tiles + v;
+    kb0 = int((int64_t(sl) * p.k_blocks) / p.splits);
+    kb1 = int((int64_t(sl + 1) * p.k_blocks) / p.splits);
+}
 
 // Cycle accounting for the diagnostics build (liblpy_trace.so); compiled out of
 // the product library.  Slots per CTA: 0 MMA total, 1 MMA wait(ready), 2 MMA
@@ -119,11 +142,12 @@ __device__ __forceinline__ void arrive_leader(uint64_t *bar) {
     else                   mbar_arrive_remote(mapa_shared(smem_u32(bar), 0));
 }
 
-template <int CG, bool AMN, bool BMN>
+template <int CG, bool AMN, bool BMN, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const Params p) {
-    using C_ = Cfg<CG>;
+    using C_ = Cfg<CG, BN>;
+    constexpr int EC = C_::EC;
     constexpr int STAGES = C_::STAGES;
     constexpr uint32_t A_BYTES = C_::A_BYTES, RAW_BYTES = C_::RAW_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
 
@@ -176,12 +200,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tma_prefetch_desc(&tmB);
                 int s = 0;
                 uint32_t ph = 0;
-                for (int t = unit0; t < p.num_tiles; t += units) {
-                    int tm, tn;
+                for (int u = unit0; u < p.num_units; u += units) {
+                    int t, kb0, kb1, su, tm, tn;
+                    unit_range(u, p, t, kb0, kb1, su);
                     tile_coords(t, p, tm, tn);
                     const int m0 = tm * (BM * CG) + rank * BM;
                     const int n0 = tn * BN + rank * C_::BN_CTA;
-                    for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    for (int kb = kb0; kb < kb1; ++kb) {
                         TR_T0(t_w);
                         mbar_wait(&empty[s], ph ^ 1);
                         TR_ADD(3, t_w);
@@ -223,10 +248,12 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint32_t ph = 0;
             uint32_t npart = 0;   // partials issued by this pair
             TR_T0(t_all);
-            for (int t = unit0; t < p.num_tiles; t += units) {
-                for (int kb = 0; kb < p.k_blocks; ++kb) {
-                    const bool first = (kb % p.promote) == 0;
-                    const bool last = (kb % p.promote) == p.promote - 1 || kb == p.k_blocks - 1;
+            for (int u = unit0; u < p.num_units; u += units) {
+                int t, kb0, kb1, su;
+                unit_range(u, p, t, kb0, kb1, su);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    const bool first = ((kb - kb0) % p.promote) == 0;
+                    const bool last = ((kb - kb0) % p.promote) == p.promote - 1 || kb == kb1 - 1;
                     const uint32_t b = npart & 1;
                     if (first) {
                         TR_T0(t_e);
@@ -268,8 +295,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         constexpr int PER_THREAD = int(RAW_BYTES / 16) / (XFORM_WARPS * 32);
         int s = 0;
         uint32_t ph = 0;
-        for (int t = unit0; t < p.num_tiles; t += units) {
-            for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int u = unit0; u < p.num_units; u += units) {
+            int t, kb0, kb1, su;
+            unit_range(u, p, t, kb0, kb1, su);
+            for (int kb = kb0; kb < kb1; ++kb) {
                 TR_T0(t_f);
                 mbar_wait(&full[s], ph);
                 TR_ADD(4, t_f);
@@ -298,12 +327,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int quad = warp & 3;                       // TMEM lanes 32*quad .. +31 (hardware rule)
         const int half = (warp - EPI_WARP0) >> 2;        // columns 128*half .. +127
         const uint32_t lane_base = uint32_t(quad * 32) << 16;
-        const int parts_per_tile = (p.k_blocks + p.promote - 1) / p.promote;
+        const int ept = threadIdx.x - EPI_WARP0 * 32;   // 0..255
+        __shared__ int last_flag;
         uint32_t np = 0;                                 // partials promoted so far
-        for (int t = unit0; t < p.num_tiles; t += units) {
-            float acc[128];
+        for (int u = unit0; u < p.num_units; u += units) {
+            int t, kb0, kb1, su;
+            unit_range(u, p, t, kb0, kb1, su);
+            const int parts_per_tile = (kb1 - kb0 + p.promote - 1) / p.promote;
+            float acc[EC];
 #pragma unroll
-            for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+            for (int j = 0; j < EC; ++j) acc[j] = 0.f;
             for (int part = 0; part < parts_per_tile; ++part, ++np) {
                 const uint32_t b = np & 1;
                 TR_T0(t_w);
@@ -311,9 +344,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 TR_ADD(5, t_w);
                 TR_T0(t_b);
                 tc_fence_after();
-                const uint32_t base = tmem + lane_base + b * 256 + half * 128;
+                const uint32_t base = tmem + lane_base + b * 256 + half * EC;
 #pragma unroll
-                for (int c = 0; c < 128; c += 32) {
+                for (int c = 0; c < EC; c += 32) {
                     uint32_t v0[16], v1[16];
                     tmem_ld_x16(base + c, v0);
                     tmem_ld_x16(base + c + 16, v1);
@@ -329,14 +362,43 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (lane == 0) arrive_leader<CG>(&acce[b]);
                 TR_ADD(7, t_b);
             }
+            if (su >= 0) {
+                // split tile: park this slice's partial (thread-interleaved float4s,
+                // a warp writes 512 contiguous bytes), count arrivals per (tile,
+                // CTA); the last slice sums all partials in slice order and stores.
+                constexpr int TILE4 = BM * BN / 4;
+                float4 *mine = reinterpret_cast<float4 *>(p.ws) + (int64_t(su) * CG + rank) * TILE4 + ept;
+#pragma unroll
+                for (int j = 0; j < EC; j += 4)
+                    __stcg(mine + (j / 4) * 256, make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
+                __threadfence();
+                named_bar_sync(1, EPI_WARPS * 32);
+                const int vt = t - p.full_tiles;
+                if (ept == 0) last_flag = (atomicAdd(p.sem + vt * CG + rank, 1) == p.splits - 1);
+                named_bar_sync(1, EPI_WARPS * 32);
+                if (!last_flag) continue;
+                __threadfence();
+                const float4 *base = reinterpret_cast<const float4 *>(p.ws) +
+                                     (int64_t(vt) * p.splits * CG + rank) * TILE4 + ept;
+#pragma unroll
+                for (int j = 0; j < EC; j += 4) {
+                    float4 a4 = __ldcg(base + (j / 4) * 256);
+                    for (int sl = 1; sl < p.splits; ++sl) {
+                        const float4 q = __ldcg(base + int64_t(sl) * CG * TILE4 + (j / 4) * 256);
+                        a4.x += q.x; a4.y += q.y; a4.z += q.z; a4.w += q.w;
+                    }
+                    acc[j] = a4.x; acc[j + 1] = a4.y; acc[j + 2] = a4.z; acc[j + 3] = a4.w;
+                }
+                if (ept == 0) p.sem[vt * CG + rank] = 0;   // ready for the next launch
+            }
             int tm, tn;
             tile_coords(t, p, tm, tn);
             const int row = tm * (BM * CG) + rank * BM + quad * 32 + lane;
             if (row < p.M) {
                 float *crow = p.C + int64_t(row) * p.ldc;
-                const int col0 = tn * BN + half * 128;
+                const int col0 = tn * BN + half * EC;
 #pragma unroll
-                for (int j = 0; j < 128; j += 4) {
+                for (int j = 0; j < EC; j += 4) {
                     const int col = col0 + j;
                     if (p.c_vec && col + 3 < p.N) {
                         *reinterpret_cast<float4 *>(crow + col) =
@@ -362,21 +424,23 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == 1) tmem_dealloc_cg<CG>(tmem, TMEM_COLS);
 }
 
-template <int CG, bool AMN, bool BMN>
+template <int CG, bool AMN, bool BMN, int BN>
 static cudaError_t launch_t(const CUtensorMap &ta, const CUtensorMap &tb, const Params &prm, int grid,
                             cudaStream_t s) {
-    auto kern = gemm_3xtf32_kernel<CG, AMN, BMN>;
+    using C_ = Cfg<CG, BN>;
+    static_assert(C_::EC % 32 == 0 && C_::SMEM_BYTES <= 227 * 1024, "tile does not fit");
+    auto kern = gemm_3xtf32_kernel<CG, AMN, BMN, BN>;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(Cfg<CG>::SMEM_BYTES));
+                                             int(C_::SMEM_BYTES));
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = Cfg<CG>::SMEM_BYTES;
+    cfg.dynamicSmemBytes = C_::SMEM_BYTES;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -390,11 +454,34 @@ static cudaError_t launch_t(const CUtensorMap &ta, const CUtensorMap &tb, const 
 
 static long long *g_trace = nullptr;   // set by lpy_trace_set_buffer (diagnostics build)
 
-template <int CG>
+// Tile width for a CTA-pair product (256-row tiles): the BN in {256, 192, 128}
+// maximising (wave efficiency of its tiles on `pairs` persistent CTA pairs) x
+// (columns not wasted by a ragged last tile) x (the kernel's measured per-flop
+// efficiency at that width relative to 256: 0.86 for 192, 0.69 for 128 at
+// n = 8192 -- narrower MMAs leave the fixed per-k-block work (the A tile's TMA
+// and split) less time to hide in; profiles/r01_tf32_bn_sweep.txt).
+// n >= 4096 -> 256; n = 1024 -> 128 (32 tiles instead of 16); the ragged
+// config -> 192 (64 tiles instead of 48).
+int choose_bn(int M, int N, int pairs) {
+    const int64_t tm = (M + 2 * BM - 1) / (2 * BM);
+    auto eff = [&](int bn) {
+        const int64_t tn = (N + bn - 1) / bn, tiles = tm * tn;
+        const int64_t waves = (tiles + pairs - 1) / pairs;
+        const double kern = bn == 256 ? 1.0 : bn == 192 ? 0.86 : 0.69;
+        return kern * double(tiles) / double(waves * pairs) * double(N) / double(tn * bn);
+    };
+    int best = 256;
+    double best_eff = eff(256);
+    for (int bn : {192, 128})
+        if (eff(bn) > best_eff * 1.03) { best = bn; best_eff = eff(bn); }
+    return best;
+}
+
+template <int CG, int BN>
 static cudaError_t launch_cg(const Problem &p, const Knobs &kn, cudaStream_t s) {
     const bool AMN = (p.la == 1);   // column-major A: M contiguous
     const bool BMN = (p.lb == 0);   // row-major B: N contiguous
-    constexpr int BN_CTA = Cfg<CG>::BN_CTA;
+    constexpr int BN_CTA = Cfg<CG, BN>::BN_CTA;
     CUtensorMap ta, tb;
     cudaError_t e;
     if (AMN) e = make_tmap_2d(&ta, p.A, p.M, p.K, p.lda, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
@@ -408,22 +495,53 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, cudaStream_t s) 
     prm.M = p.M; prm.N = p.N; prm.K = p.K;
     prm.C = p.C; prm.ldc = p.ldc;
     prm.tiles_m = (p.M + BM * CG - 1) / (BM * CG);
-    prm.tiles_n = (p.N + BN - 1) / BN;
+    prm.tiles_n = (p.N + BN - 1) / BN;   // (template BN)
     prm.num_tiles = prm.tiles_m * prm.tiles_n;
     prm.k_blocks = (p.K + BK - 1) / BK;
     prm.group = kn.raster_group > 0 ? kn.raster_group : 16 / CG;
     prm.promote = kn.promote_kblocks > 0 ? kn.promote_kblocks : 8;   // 128 of K per TMEM partial
     prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
     prm.trace = g_trace;
+    // Tail split, fixed by the shape and the device (never by opts.num_ctas, so
+    // results stay bitwise grid-invariant): when the last of >= 2 waves is
+    // partial, its `rem` tiles are cut into S = floor(pairs / rem) k-slices
+    // (<= 4, >= 16 k-blocks each) so the last wave is S times shorter.
+    {
+        const int pairs = kn.num_sms / CG;
+        const int waves = (prm.num_tiles + pairs - 1) / pairs;
+        const int rem = prm.num_tiles - (waves - 1) * pairs;
+        int S = rem > 0 ? pairs / rem : 1;
+        if (S > 4) S = 4;
+        while (S > 1 && prm.k_blocks / S < 16) --S;
+        if (waves < 2 || S < 2) S = 1;
+        prm.splits = S;
+        prm.full_tiles = S > 1 ? (waves - 1) * pairs : prm.num_tiles;
+        prm.num_units = prm.full_tiles + (prm.num_tiles - prm.full_tiles) * S;
+    }
+    prm.ws = nullptr;
+    prm.sem = nullptr;
     int units = (kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms) / CG;  // CTAs (pairs) in the grid
-    if (units > prm.num_tiles) units = prm.num_tiles;
+    if (units > prm.num_units) units = prm.num_units;
     if (units < 1) units = 1;
     const int grid = units * CG;
+    if (prm.splits > 1) {
+        const int split_tiles = prm.num_tiles - prm.full_tiles;
+        const size_t ws_bytes = size_t(split_tiles) * prm.splits * CG * BM * BN * 4;
+        char *buf = nullptr;
+        e = cudaMallocAsync(reinterpret_cast<void **>(&buf), ws_bytes + size_t(split_tiles) * CG * 4, s);
+        if (e != cudaSuccess) return e;
+        prm.ws = reinterpret_cast<float *>(buf);
+        prm.sem = reinterpret_cast<int *>(buf + ws_bytes);
+        e = cudaMemsetAsync(prm.sem, 0, size_t(split_tiles) * CG * 4, s);
+        if (e != cudaSuccess) { cudaFreeAsync(buf, s); return e; }
+    }
 
-    if (AMN && BMN)  return launch_t<CG, true, true>(ta, tb, prm, grid, s);
-    if (AMN && !BMN) return launch_t<CG, true, false>(ta, tb, prm, grid, s);
-    if (!AMN && BMN) return launch_t<CG, false, true>(ta, tb, prm, grid, s);
-    return launch_t<CG, false, false>(ta, tb, prm, grid, s);
+    if (AMN && BMN)       e = launch_t<CG, true, true, BN>(ta, tb, prm, grid, s);
+    else if (AMN && !BMN) e = launch_t<CG, true, false, BN>(ta, tb, prm, grid, s);
+    else if (!AMN && BMN) e = launch_t<CG, false, true, BN>(ta, tb, prm, grid, s);
+    else                  e = launch_t<CG, false, false, BN>(ta, tb, prm, grid, s);
+    if (prm.ws) cudaFreeAsync(prm.ws, s);
+    return e;
 }
 
 }  // namespace tf32
@@ -437,7 +555,17 @@ cudaError_t launch_3xtf32(const Problem &p, const Knobs &kn, cudaStream_t s) {
         const char *e = getenv("LPY_TF32_CG");
         return (e && e[0] == '1') ? 1 : 2;
     }();
-    return cg == 1 ? tf32::launch_cg<1>(p, kn, s) : tf32::launch_cg<2>(p, kn, s);
+    if (cg == 1) return tf32::launch_cg<1, 256>(p, kn, s);
+    // LPY_TF32_BN=128|192|256 forces the tile width (diagnostics / A-B comparison).
+    static const int force_bn = [] {
+        const char *e = getenv("LPY_TF32_BN");
+        return e ? atoi(e) : 0;
+    }();
+    switch (force_bn ? force_bn : tf32::choose_bn(p.M, p.N, kn.num_sms / 2)) {
+        case 128: return tf32::launch_cg<2, 128>(p, kn, s);
+        case 192: return tf32::launch_cg<2, 192>(p, kn, s);
+        default:  return tf32::launch_cg<2, 256>(p, kn, s);
+    }
 }
 
 }  // namespace lpy

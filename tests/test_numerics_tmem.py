@@ -120,7 +120,7 @@ def test_uniform_accumulation_error(probe):
 
 def test_mma_rate(probe):
     cyc = torch.zeros(1, dtype=torch.int64, device="cuda")
-    for n in (128, 256):
+    for n in (128, 160, 192, 224, 256):
         for ctas in (1, 148):
             probe.lpy_probe_umma_rate(n, 2000, ctas, cyc.data_ptr(), None)
             torch.cuda.synchronize()
