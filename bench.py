@@ -188,7 +188,9 @@ def run_reference(args, rank, world):
         return
     import oracle
     n = args.n
-    per_step = max(0.5, args.ref_seconds)
+    # each step a bounded sample: the whole --steps K --warmup W run stays near
+    # --ref-total seconds (a few minutes at most), at least 0.2 s of work per step
+    per_step = max(0.2, min(args.ref_seconds, args.ref_total / max(1, args.steps + args.warmup)))
     # calibrate the sample once, then time each step on that fixed sample
     gf, dt, sample, threads = oracle_sample(n, per_step, "uniform")
     times = []
@@ -503,7 +505,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--ref-seconds", type=float, default=4.0)
+    ap.add_argument("--ref-seconds", type=float, default=4.0, help="--impl reference: max seconds per step")
+    ap.add_argument("--ref-total", type=float, default=120.0, help="--impl reference: target seconds for the run")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
