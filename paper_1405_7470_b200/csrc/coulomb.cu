@@ -13,6 +13,10 @@
 //   * sources are packed once into float4 (x, y, z, q) and streamed through
 //     shared memory in tiles of 256 (one 16-byte broadcast LDS per source per
 //     thread), double-buffered;
+//   * coincident points (r = 0, excluded) are masked only where they can occur
+//     for sure -- the tiles holding a CTA's own targets in a self-potential --
+//     and any other coincidence shows up as a non-finite sum, which sends that
+//     target down a scalar masked path: the hot loop carries no select;
 //   * each thread owns 4 targets held as two packed pairs, so the r^2 and
 //     accumulation arithmetic runs as FADD2 / FMUL2 / FFMA2 (two fp32 RN ops per
 //     instruction), leaving the 16-per-clock-per-SM MUFU.RSQ as the bound;
@@ -89,6 +93,63 @@ __device__ __forceinline__ void kahan2(u64 &sum, u64 &comp, u64 x) {
     sum = t;
 }
 
+// One chunk of CHUNK sources from shared memory into the pair accumulators.
+// MASK: exclude coincident points with a select (FSETP + FSEL per target);
+// without it a coincident pair yields inf / NaN, which the caller detects.
+template <bool MASK, int NP>
+__device__ __forceinline__ void chunk_pass(const float4 *__restrict__ src, const u64 (&xp)[NP],
+                                           const u64 (&yp)[NP], const u64 (&zp)[NP], u64 (&ap)[NP]) {
+#pragma unroll 8
+    for (int j = 0; j < CHUNK; ++j) {
+        const float4 sj = src[j];
+#pragma unroll
+        for (int h = 0; h < NP; ++h) {
+            const u64 dx = sub2s(xp[h], sj.x), dy = sub2s(yp[h], sj.y), dz = sub2s(zp[h], sj.z);
+            u64 r2 = mul2(dx, dx);
+            r2 = fma2(dy, dy, r2);
+            r2 = fma2(dz, dz, r2);
+            float q0, q1;
+            upk(r2, q0, q1);
+            float r0, r1;
+            asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(q0));
+            asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(q1));
+            if constexpr (MASK) {
+                r0 = q0 > 0.f ? r0 : 0.f;
+                r1 = q1 > 0.f ? r1 : 0.f;
+            }
+            ap[h] = fma2s(sj.w, pk(r0, r1), ap[h]);
+        }
+    }
+}
+
+// The same sum for one target, scalar and masked, over source tiles
+// [tile0, tile1) read from global memory: the rare path for a target that
+// coincides with a source outside the tiles the main loop masks.  Every
+// operation is the lane-wise equivalent of the packed one, so the result is
+// bitwise the one the masked packed loop gives.
+__device__ __noinline__ float target_sum_masked(float x, float y, float z, const float4 *__restrict__ src4, int tile0,
+                                   int tile1) {
+    float sum = 0.f, comp = 0.f;
+    for (int tl = tile0; tl < tile1; ++tl) {
+        for (int c0 = 0; c0 < TILE; c0 += CHUNK) {
+            float a = 0.f;
+            for (int j = 0; j < CHUNK; ++j) {
+                const float4 sj = src4[int64_t(tl) * TILE + c0 + j];
+                const float dx = x - sj.x, dy = y - sj.y, dz = z - sj.z;
+                float r2 = __fmul_rn(dx, dx);
+                r2 = __fmaf_rn(dy, dy, r2);
+                r2 = __fmaf_rn(dz, dz, r2);
+                a = __fmaf_rn(sj.w, rinv(r2), a);
+            }
+            const float yk = __fsub_rn(a, comp);
+            const float tk = __fadd_rn(sum, yk);
+            comp = __fsub_rn(__fsub_rn(tk, sum), yk);
+            sum = tk;
+        }
+    }
+    return __fsub_rn(sum, comp);
+}
+
 // Packed sources: src4[j] = (x, y, z, q); entries ns .. ns_pad-1 are q = 0 at FAR.
 __global__ void pack_kernel(int64_t ns, int64_t ns_pad, const float *__restrict__ s, int64_t lds,
                             const float *__restrict__ q, float4 *__restrict__ src4) {
@@ -102,7 +163,7 @@ __global__ void pack_kernel(int64_t ns, int64_t ns_pad, const float *__restrict_
 // written directly; else partial[slice][i].
 __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     potential_kernel(int64_t nt, const float *__restrict__ t, int64_t ldt, const float4 *__restrict__ src4,
-                     int ntiles, int splits, float *__restrict__ phi, float *__restrict__ partial) {
+                     int ntiles, int splits, int self, float *__restrict__ phi, float *__restrict__ partial) {
     __shared__ float4 tile[2][TILE];
     const int tb = blockIdx.x / splits, sl = blockIdx.x - tb * splits;
     const int tile0 = int((int64_t(sl) * ntiles) / splits), tile1 = int((int64_t(sl + 1) * ntiles) / splits);
@@ -132,28 +193,21 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
 
     if (tile0 < tile1) tile[0][threadIdx.x] = src4[int64_t(tile0) * TILE + threadIdx.x];
     __syncthreads();
+    // self-potential (targets are the sources): this CTA's own targets sit in
+    // source tiles [diag0, diag1); only those need the coincidence mask
+    const int diag0 = self ? tb * (THREADS * TPT / TILE) : 0;
+    const int diag1 = self ? diag0 + THREADS * TPT / TILE : 0;
     for (int tl = tile0; tl < tile1; ++tl) {
         const int b = (tl - tile0) & 1;
         if (tl + 1 < tile1) tile[b ^ 1][threadIdx.x] = src4[int64_t(tl + 1) * TILE + threadIdx.x];
+        const bool masked = tl >= diag0 && tl < diag1;
 #pragma unroll 1
         for (int c0 = 0; c0 < TILE; c0 += CHUNK) {
             u64 ap[NP];
 #pragma unroll
             for (int h = 0; h < NP; ++h) ap[h] = 0;
-#pragma unroll 8
-            for (int j = c0; j < c0 + CHUNK; ++j) {
-                const float4 sj = tile[b][j];
-#pragma unroll
-                for (int h = 0; h < NP; ++h) {
-                    const u64 dx = sub2s(xp[h], sj.x), dy = sub2s(yp[h], sj.y), dz = sub2s(zp[h], sj.z);
-                    u64 r2 = mul2(dx, dx);
-                    r2 = fma2(dy, dy, r2);
-                    r2 = fma2(dz, dz, r2);
-                    float q0, q1;
-                    upk(r2, q0, q1);
-                    ap[h] = fma2s(sj.w, pk(rinv(q0), rinv(q1)), ap[h]);
-                }
-            }
+            if (masked) chunk_pass<true, NP>(&tile[b][c0], xp, yp, zp, ap);
+            else        chunk_pass<false, NP>(&tile[b][c0], xp, yp, zp, ap);
 #pragma unroll
             for (int h = 0; h < NP; ++h) kahan2(sp[h], cp[h], ap[h]);
         }
@@ -167,6 +221,9 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     for (int k = 0; k < TPT; ++k) {
         const int64_t i = base + int64_t(k) * THREADS;
         if (i >= nt) continue;
+        // a coincident point outside the masked tiles made this sum inf / NaN:
+        // redo the target with the mask everywhere (bitwise what the masked loop gives)
+        if (!isfinite(r[k])) r[k] = target_sum_masked(tx[k], ty[k], tz[k], src4, tile0, tile1);
         if (splits == 1) phi[i] = r[k];
         else             partial[int64_t(sl) * nt + i] = r[k];
     }
@@ -214,8 +271,9 @@ cudaError_t launch_coulomb(int64_t nt, const float *t, int64_t ldt, int64_t ns, 
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) {
+        const int self = (t == s && ldt == lds && nt == ns) ? 1 : 0;
         potential_kernel<<<unsigned(blocks_t * splits), THREADS, 0, st>>>(nt, t, ldt, src4, int(ntiles), splits,
-                                                                         phi, partial);
+                                                                         self, phi, partial);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess && splits > 1) {

@@ -360,3 +360,64 @@ extern "C" int lpy_probe_rsqrt_eval(const float *in, float *out, int n, void *st
     lpy::probe::rsqrt_eval_kernel<<<592, 256, 0, static_cast<cudaStream_t>(stream)>>>(in, out, n);
     return int(cudaGetLastError());
 }
+
+// ---------------------------------------------------------------- f32x2 rates
+// 8 independent chains per thread of one packed instruction kind:
+// 0 fma.rn.f32x2, 1 add.rn.f32x2, 2 mul.rn.f32x2, 3 scalar add.f32 (16 chains),
+// 4 scalar fma.f32 (16 chains).  Lane-ops per second = 16 * iters * threads / time.
+namespace lpy {
+namespace probe {
+template <int KIND>
+__global__ void x2_rate_kernel(float *out, int iters, float x) {
+    unsigned long long a[8];
+    float f[16];
+    unsigned long long xx;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(x));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float lo = threadIdx.x * 1e-3f + j, hi = lo + 0.5f;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(a[j]) : "f"(lo), "f"(hi));
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) f[j] = threadIdx.x * 1e-3f + j;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if constexpr (KIND == 0) asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(a[j]) : "l"(xx));
+            if constexpr (KIND == 1) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(a[j]) : "l"(xx));
+            if constexpr (KIND == 2) asm volatile("mul.rn.f32x2 %0, %0, %1;" : "+l"(a[j]) : "l"(xx));
+        }
+        if constexpr (KIND == 3) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) asm volatile("add.rn.f32 %0, %0, %1;" : "+f"(f[j]) : "f"(x));
+        }
+        if constexpr (KIND == 4) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) asm volatile("fma.rn.f32 %0, %0, %1, %1;" : "+f"(f[j]) : "f"(x));
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float lo, hi;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a[j]));
+        s += lo + hi;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s += f[j];
+    if (s == 12345.678f) out[0] = s;
+}
+}  // namespace probe
+}  // namespace lpy
+
+extern "C" int lpy_probe_x2_rate(int kind, float *out, int iters, int blocks, int threads, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (kind) {
+        case 0: lpy::probe::x2_rate_kernel<0><<<blocks, threads, 0, s>>>(out, iters, 0.999f); break;
+        case 1: lpy::probe::x2_rate_kernel<1><<<blocks, threads, 0, s>>>(out, iters, 0.999f); break;
+        case 2: lpy::probe::x2_rate_kernel<2><<<blocks, threads, 0, s>>>(out, iters, 0.999f); break;
+        case 3: lpy::probe::x2_rate_kernel<3><<<blocks, threads, 0, s>>>(out, iters, 0.999f); break;
+        default: lpy::probe::x2_rate_kernel<4><<<blocks, threads, 0, s>>>(out, iters, 0.999f); break;
+    }
+    return int(cudaGetLastError());
+}

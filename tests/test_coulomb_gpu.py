@@ -124,6 +124,21 @@ def test_closed_forms_and_exclusion():
     check(on, p[k:k + 1], p[keep], q[keep])
 
 
+def test_duplicate_positions_far_apart():
+    """Two particles at the same position with distant indices (different
+    source tiles, outside the masked diagonal tiles of a self-potential): each
+    excludes the other -- the non-finite fallback path -- and the other targets
+    are unaffected."""
+    p, q = cloud(5000, 11)
+    p[4321] = p[17]
+    phi, _ = run_coulomb(p, p, q)
+    check(phi, p, p, q)
+    t = np.concatenate([p[17:18], p[:3]])       # separate target set, first target on two sources
+    phi2, _ = run_coulomb(t, p, q)
+    check(phi2, t, p, q)
+    assert phi2[0] == phi[17]
+
+
 def test_determinism_and_scaling():
     p, q = cloud(20000, 8)
     a, _ = run_coulomb(p, p, q)

@@ -206,3 +206,25 @@ def test_rsqrt_accuracy(probe):
     RESULTS["rsqrt_max_rel_err_log2"] = float(np.log2(rel.max()))
     print(RESULTS)
     assert rel.max() < 2.0 ** -21
+
+
+def test_f32x2_rates(probe):
+    """Per-SM lane-op throughput of packed fp32 (FFMA2 / FADD2 / FMUL2) and of
+    scalar FADD / FFMA at the 1.965 GHz max clock: which FMA-pipe half the
+    packed forms use (the Coulomb kernel's r^2 arithmetic)."""
+    probe.lpy_probe_x2_rate.argtypes = [ctypes.c_int, ctypes.c_void_p] + [ctypes.c_int] * 3 + [ctypes.c_void_p]
+    out = torch.zeros(1, device="cuda")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    iters, blocks, threads = 20000, sms * 4, 256
+    for kind, name in enumerate(["ffma2", "fadd2", "fmul2", "fadd", "ffma"]):
+        probe.lpy_probe_x2_rate(kind, out.data_ptr(), 100, blocks, threads, None)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        probe.lpy_probe_x2_rate(kind, out.data_ptr(), iters, blocks, threads, None)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        lane_ops = 16.0 * iters * blocks * threads
+        RESULTS[f"{name}_lane_ops_per_clk_per_sm"] = lane_ops / (ms * 1e-3) / sms / 1.965e9
+    print(RESULTS)
