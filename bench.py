@@ -244,19 +244,23 @@ def make_inputs(n, rank, world, chunks, device):
 def time_path(args, path, rank, world, device, dist_on):
     import torch
     import paper_1405_7470_b200 as lpy
-    from paper_1405_7470_b200.dist import choose_chunks, panel_bounds, rowpanel_gemm
+    from paper_1405_7470_b200.dist import choose_chunks, chunk_grid, chunk_streams, panel_bounds, rowpanel_gemm
     n = args.n
-    r0_, r1_ = panel_bounds(n, world, rank)
-    chunks = (args.chunks or choose_chunks(r1_ - r0_, n,
-                                            torch.cuda.get_device_properties(device).multi_processor_count)
-              ) if dist_on else 1
-    A, blocks, C, bounds, (r0, r1) = make_inputs(n, rank, world, chunks, device)
+    pw = args.emulate_ranks if (args.emulate_ranks and world == 1) else world   # panel split
+    r0_, r1_ = panel_bounds(n, pw, rank)
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    chunks = (args.chunks or choose_chunks(r1_ - r0_, n, sms)) if dist_on else 1
+    A, blocks, C, bounds, (r0, r1) = make_inputs(n, rank, pw, chunks, device)
 
     def gemm_fn(a, b, c):
-        lpy.gemm(a, b, out=c, path=path)
+        opts = None
+        if dist_on and len(bounds) > 1:
+            opts = lpy.GemmOpts()
+            opts.num_ctas = chunk_grid(a.shape[0], b.shape[1], sms, path)
+        lpy.gemm(a, b, out=c, path=path, opts=opts)
 
     comm = torch.cuda.Stream() if dist_on else None
-    cstreams = [torch.cuda.Stream(), torch.cuda.Stream()] if dist_on else None
+    cstreams = [torch.cuda.Stream() for _ in range(chunk_streams(r1 - r0, len(bounds)))] if dist_on else None
 
     def step():
         if not dist_on:
@@ -500,6 +504,8 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "ffma", "3xtf32"])
     ap.add_argument("--also", default="ffma", help="secondary path to report ('' for none)")
     ap.add_argument("--chunks", type=int, default=0, help="B column blocks for N>1 (0 = ~1 wave each)")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="diagnostics at N=1 with --force-dist: rank 0's panel of an N-rank split (not a bench value)")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the row-panel + NCCL broadcast step even at N=1 (exercises the N>1 path)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -12,10 +12,10 @@ storage: `chunks` contiguous blocks, block c a row-major K x w_c matrix
 Block c is broadcast on a dedicated communication stream; as soon as it has
 arrived, C[:, cols_c] = A_panel B_c (an lpy_gemm_f32 call writing a disjoint
 column block of C, ldc = N) runs on one of `compute_streams` streams, so the
-product of a block overlaps the broadcast of the next and, when one block's
-product does not fill the GPU, two blocks' products share it.  Chunk widths are
+product of a block overlaps the broadcast of the next, and the block products
+run concurrently on several streams, each with a persistent grid sized to its
+own tiles (`chunk_grid`), so together they fill the GPU.  Chunk widths are
 multiples of 256 (the 3xTF32 pair tile) so each block is 16-byte aligned.
-`choose_chunks` sizes blocks to about one wave of output tiles.
 
 The GEMM itself is injected (`gemm_fn`) so the orchestration can be tested
 on CPU with the gloo backend (tests/test_dist.py).
@@ -49,10 +49,32 @@ def chunk_bounds(N: int, chunks: int, align: int = 256) -> list[tuple[int, int]]
 
 
 def choose_chunks(rows: int, N: int, sms: int = 148, tile: int = 256, max_chunks: int = 8) -> int:
-    """Number of B column blocks for a rank's (rows x N) panel: about one wave of
-    256 x 256 output tiles per block on `sms` SMs (CTA pairs), at least 1."""
-    tiles = math.ceil(rows / tile) * math.ceil(N / tile)
-    return max(1, min(max_chunks, tiles // max(1, sms // 2)))
+    """Number of B column blocks for a rank's (rows x N) panel.  The step takes
+    about T_bcast / chunks + T_products(chunks); measured on one B200 at n=8192
+    (scripts/panel_probe.py, profiles/r01_panel_probe.txt) the products lose
+    2-3% at 8 blocks for a 1024-row panel but 8-11% for 2048/4096-row panels,
+    where the broadcast is also a smaller share of the step, so: 8 blocks for
+    panels of <= 1024 rows, 4 up to 2048, else 2 (blocks >= 1024 columns)."""
+    del sms
+    want = 8 if rows <= 1024 else 4 if rows <= 2048 else 2
+    return max(1, min(max_chunks, want, N // (4 * tile)))
+
+
+def chunk_streams(rows: int, chunks: int) -> int:
+    """Concurrent compute streams for the block products (same measurement):
+    4 for 1024-row panels, 2 up to 2048, 1 beyond (then one block's product
+    fills the GPU by itself)."""
+    want = 4 if rows <= 1024 else 2 if rows <= 2048 else 1
+    return max(1, min(want, chunks))
+
+
+def chunk_grid(rows: int, cols: int, sms: int, path: str) -> int:
+    """Persistent grid (CTAs) for one block product sized to its own tiles
+    (256 x 256 per CTA pair on 3xTF32, 128 x 128 per CTA on FFMA), so
+    concurrent block products share the SMs instead of each claiming all."""
+    if path == "3xtf32":
+        return 2 * max(1, min(sms // 2, math.ceil(rows / 256) * math.ceil(cols / 256)))
+    return max(1, min(sms, math.ceil(rows / 128) * math.ceil(cols / 128)))
 
 
 def rowpanel_gemm(A_panel, B_blocks, C_panel, bounds, group=None, root=0, gemm_fn=None,
@@ -87,7 +109,8 @@ def rowpanel_gemm(A_panel, B_blocks, C_panel, bounds, group=None, root=0, gemm_f
 
     caller = torch.cuda.current_stream()
     comm = comm_stream or torch.cuda.Stream()
-    streams = compute_streams or [torch.cuda.Stream(), torch.cuda.Stream()]
+    streams = compute_streams or [torch.cuda.Stream()
+                                  for _ in range(chunk_streams(A_panel.shape[0], len(B_blocks)))]
     comm.wait_stream(caller)
     for st in streams:
         st.wait_stream(caller)

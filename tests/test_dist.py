@@ -13,7 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1405_7470_b200.dist import chunk_bounds, panel_bounds, rowpanel_gemm
+from paper_1405_7470_b200.dist import (chunk_bounds, chunk_grid, chunk_streams, choose_chunks, panel_bounds,
+                                       rowpanel_gemm)
 
 
 def test_panel_bounds_cover_rows_exactly():
@@ -38,6 +39,18 @@ def test_chunk_bounds_aligned_and_covering():
             assert len(b) <= max(1, c)
     assert chunk_bounds(8192, 4) == [(0, 2048), (2048, 4096), (4096, 6144), (6144, 8192)]
     assert chunk_bounds(0, 4) == []
+
+
+def test_chunk_policy():
+    # n = 8192 panels for g = 8 / 4 / 2 / 1 ranks
+    assert [choose_chunks(8192 // g, 8192) for g in (8, 4, 2, 1)] == [8, 4, 2, 2]
+    assert [chunk_streams(8192 // g, choose_chunks(8192 // g, 8192)) for g in (8, 4, 2, 1)] == [4, 2, 1, 1]
+    assert choose_chunks(1024, 1000) == 1 and choose_chunks(1024, 0) == 1
+    # grids sized to a block's own tiles, never beyond the chip
+    assert chunk_grid(1024, 1024, 148, "3xtf32") == 32      # 16 pair tiles
+    assert chunk_grid(8192, 8192, 148, "3xtf32") == 148
+    assert chunk_grid(1024, 1024, 148, "ffma") == 64
+    assert chunk_grid(1, 1, 148, "ffma") == 1
 
 
 def _free_port():
