@@ -415,16 +415,16 @@ def time_saxpy(args, device):
     for _ in range(args.warmup):
         lpy.saxpy(alpha, x, y)
     torch.cuda.synchronize()
-    per = []
+    # back-to-back calls between one pair of events on the launching stream:
+    # the mean per-call time (per-call event pairs add their own gaps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(stream)
         for _ in range(args.steps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
             lpy.saxpy(alpha, x, y)
-            e1.record(stream)
-            per.append((e0, e1))
+        e1.record(stream)
         torch.cuda.synchronize()
-    ms = statistics.mean(a.elapsed_time(b) for a, b in per)
+    ms = e0.elapsed_time(e1) / args.steps
     gbs = 12.0 * n / (ms * 1e-3) / 1e9
     peaks, src = load_peaks()
     peak = peaks["hbm_gbs"]
