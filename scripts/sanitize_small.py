@@ -29,3 +29,49 @@ for path in ("ffma", "3xtf32"):
         assert pad_ok
         worst = max(worst, check(C, A, B))
 print(f"sanitize_small: all products within tolerance (worst {worst:.2e})")
+
+# split-K FFMA (under-filled grid: 72 tiles -> 2 slices) and the 3xTF32 tail
+# split (90 pair tiles = 2 waves, the last 16 cut into k-slices)
+import paper_1405_7470_b200 as lpy  # noqa: E402
+import oracle  # noqa: E402
+import torch  # noqa: E402
+for path, (M, N, K) in (("ffma", (1000, 1100, 600)), ("3xtf32", (2560, 2304, 1024))):
+    A = synth.matrix(M, K, seed=5, matrix_id=0)
+    B = synth.matrix(K, N, seed=5, matrix_id=1)
+    C, pad_ok = run_gemm(A, B, 0, 0, 0, path=path)
+    assert pad_ok
+    worst = max(worst, check(C, A, B))
+print(f"sanitize_small: split products within tolerance (worst {worst:.2e})")
+
+# saxpy edges (head / tail, misaligned x, x == y, strided)
+for n, offx, offy in ((1, 0, 0), (13, 1, 3), (1001, 2, 0), (4099, 0, 5)):
+    x = synth.vector(n, 1, synth.VECTOR_X)
+    y = synth.vector(n, 1, synth.VECTOR_Y)
+    tx = torch.zeros(n + 8, device="cuda")
+    ty = torch.zeros(n + 8, device="cuda")
+    tx[offx:offx + n] = torch.from_numpy(x)
+    ty[offy:offy + n] = torch.from_numpy(y)
+    lpy.saxpy(1.5, tx[offx:offx + n], ty[offy:offy + n])
+    torch.cuda.synchronize()
+    assert oracle.saxpy_error_ulps(ty[offy:offy + n].cpu().numpy(), oracle.saxpy(n, 1.5, x, 1, y, 1)) <= 1
+tz = torch.from_numpy(synth.vector(777, 2)).cuda()
+lpy.saxpy(0.5, tz[::3], tz[::3])
+torch.cuda.synchronize()
+print("sanitize_small: saxpy edges ok")
+
+# Coulomb: self-potential with source slices, separate sets, the coincident fallback
+for nt, ns in ((300, 300), (7, 2000), (1500, 1500)):
+    pos, q = synth.particles(max(nt, ns), 3)
+    P = torch.from_numpy(pos.reshape(-1, 3)).cuda()
+    Q = torch.from_numpy(q).cuda()
+    if nt == ns:
+        phi = lpy.coulomb(P[:nt], P[:ns], Q[:ns])
+        ref, D = oracle.coulomb(nt, pos[:3 * nt].copy(), 3, ns, pos[:3 * ns].copy(), 3, q[:ns].copy())
+    else:
+        T = P[ns - nt:ns].clone()          # targets on top of sources: the fallback path
+        phi = lpy.coulomb(T, P[:ns], Q[:ns])
+        ref, D = oracle.coulomb(nt, pos[3 * (ns - nt):3 * ns].copy(), 3, ns, pos[:3 * ns].copy(), 3,
+                                q[:ns].copy())
+    torch.cuda.synchronize()
+    assert np.max(np.abs(phi.cpu().numpy() - ref) / D) <= 5e-6
+print("sanitize_small: coulomb ok")
