@@ -386,6 +386,47 @@ def time_e2e(args, path, rank, world, device):
             "d2h_bytes_per_step": d2h, "ms_per_step": ms}
 
 
+def time_cublas_context(args, device):
+    """Context only: torch.matmul on the same n x n fp32 inputs
+    through cuBLAS as SGEMM (allow_tf32 = False, fp32-accurate) and as plain
+    TF32 (allow_tf32 = True, NOT fp32-accurate: its normalised error is
+    reported beside it).  Library kernels, not this repository's."""
+    import numpy as np
+    import torch
+    import oracle
+    n = args.n
+    g = torch.Generator(device=device)
+    g.manual_seed(0)
+    A = torch.rand(n, n, device=device, generator=g) * 2 - 1
+    B = torch.rand(n, n, device=device, generator=g) * 2 - 1
+    out = {}
+    rows = np.arange(0, n, max(1, n // 64))
+    Ah = A[rows].cpu().numpy().reshape(-1)
+    Bh = B.cpu().numpy().reshape(-1)
+    Cref, D = oracle.gemm_rows(len(rows), n, n, Ah, n, 0, Bh, n, 0)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    try:
+        for name, tf32 in (("cublas_sgemm", False), ("cublas_tf32", True)):
+            torch.backends.cuda.matmul.allow_tf32 = tf32
+            for _ in range(3):
+                C = A @ B
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 10
+            e0.record()
+            for _ in range(reps):
+                C = A @ B
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            err = oracle.normalized_error(C[rows].cpu().numpy(), Cref, D)
+            out[name] = {"tflops": round(2.0 * n ** 3 / (ms * 1e-3) / 1e12, 2), "ms": round(ms, 4),
+                         "max_norm_err_sampled_rows": err}
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return out
+
+
 def time_saxpy(args, device):
     """Table 1's saxpy row: y := alpha*x + y over n = 2^28
     fp32 elements (1 GiB per vector, 3 GiB of HBM traffic per call, far above
@@ -518,6 +559,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--saxpy-n", type=int, default=1 << 28, help="saxpy length (0 = skip the saxpy line)")
     ap.add_argument("--coulomb-n", type=int, default=1 << 16, help="Coulomb particles (0 = skip)")
+    ap.add_argument("--no-context", action="store_true", help="skip the cuBLAS context timings")
     args = ap.parse_args()
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
 
@@ -554,6 +596,7 @@ def main():
     e2e = None if args.no_e2e else time_e2e(args, main_path, rank, world, device)
     sax = time_saxpy(args, device) if (args.saxpy_n > 0 and rank == 0 and not dist_on) else None
     coul = time_coulomb(args, device) if (args.coulomb_n > 0 and rank == 0 and not dist_on) else None
+    ctx = time_cublas_context(args, device) if (not args.no_context and rank == 0 and not dist_on) else None
 
     if rank == 0:
         n = args.n
@@ -602,6 +645,8 @@ def main():
             line["saxpy"] = sax
         if coul is not None:
             line["coulomb"] = coul
+        if ctx is not None:
+            line["context_cublas"] = ctx
         if also is not None:
             ams = also["total_ms"] / args.steps
             line["alt_path"] = {"path": also["path"], "value": round(flops / (ams * 1e-3) / 1e9, 1),
