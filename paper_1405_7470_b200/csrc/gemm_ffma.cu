@@ -6,15 +6,16 @@
 // (P:621-632), unrolling ("unr") and instruction-level parallelism
 // ("ilp").  The sm_100a realisation:
 //
-//   * split i -> (tile_m, m in tile), j -> (tile_n, n in tile): 128x128 output
-//     tiles, distributed over a PERSISTENT grid (one CTA per SM) in grouped
-//     raster order so concurrently running tiles share A/B panels in L2;
+//   * split i -> (tile_m, m in tile), j -> (tile_n, n in tile): 128 x 256 (or
+//     128 x 128 when that fills the waves better) output tiles, distributed over
+//     a PERSISTENT grid (one CTA per SM) in grouped raster order so
+//     concurrently running tiles share A/B panels in L2;
 //   * split k -> (k_block, k in block), BK = 32: the "prefetch" of A[tile,kb]
 //     and B[kb,tile] is one TMA (cp.async.bulk.tensor) per operand per k-block
 //     into a shared-memory ring guarded by full/empty mbarriers (producer warp
 //     <-> consumer warps) instead of work-group barriers;
-//   * ilp + unr: each consumer thread owns an 8x8 register micro-tile and runs
-//     the k loop fully unrolled; operands come from shared memory as LDS.128
+//   * ilp + unr: each consumer thread owns an 8 x 16 (or 8 x 8) register
+//     micro-tile and runs the k loop fully unrolled; operands come from shared memory as LDS.128
 //     fragments with in-warp broadcast, and the products are packed FFMA2
 //     (fma.rn.f32x2: two fp32 RN FMAs per instruction, a scalar of A times a
 //     pair of adjacent B columns);
@@ -39,18 +40,21 @@
 namespace lpy {
 namespace ffma {
 
-constexpr int BM = 128, BN = 128, BK = 32;   // (BK = 64 with 3 stages measured no faster)
+constexpr int BM = 128, BK = 32;             // tile width BN: template (128 or 256)
 constexpr int KSUB = 32;                     // k per 128B-swizzled K-major TMA box (= BK)
-constexpr int CWARPS = 8;                    // consumer warps: 2 along m (64 rows) x 4 along n (32 cols)
+constexpr int CWARPS = 8;                    // consumer warps: 2 along m (64 rows) x 4 along n (BN/4 cols)
 constexpr int XWARPS = 3;                    // transpose warps (warps CWARPS+1 .. CWARPS+3)
 
 // Per-layout geometry.  AK: A is K-major (row-major A); BKM: B is K-major
 // (column-major B).  Each stage holds the raw TMA tiles plus MN-major copies
 // of the K-major ones.
-template <bool AK, bool BKM>
+template <bool AK, bool BKM, int BN>
 struct Geo {
     static constexpr bool XA = AK, XB = BKM, X = AK || BKM;
-    static constexpr int STAGES = (AK && BKM) ? 3 : 4;
+    static constexpr int JN = BN / 32;                     // column pairs per thread (8 x 2JN micro-tile)
+    static constexpr int STAGE_FLOATS_ = BM * BK + BN * BK + (XA ? BM * BK : 0) + (XB ? BN * BK : 0);
+    static constexpr int STAGES_FIT = int((227 * 1024 - 1024 - 256) / (STAGE_FLOATS_ * 4));
+    static constexpr int STAGES = STAGES_FIT < 4 ? STAGES_FIT : 4;
     // 8 consumer warps + a producer warpgroup (warp CWARPS: one TMA lane; the next
     // XWARPS warps: transposes).  A whole warpgroup so setmaxnreg can move its
     // registers to the consumers: launched at 168/thread (the SMSP holding 3
@@ -113,31 +117,32 @@ __device__ __forceinline__ void tile_coords(int t, const Params &p, int &tm, int
     tn = r / gsize;
 }
 
-// Row (within the tile) of this thread's i-th accumulator row, column of its j-th.
+// Row (within the tile) of this thread's i-th accumulator row, column of its j-th:
+// 8 rows (two groups of 4 adjacent, 32 apart) x 2JN columns (groups of 4
+// adjacent, 16 apart) -- every fragment is one conflict-free LDS.128 per group.
 __device__ __forceinline__ int a_row(int wm, int lm, int i) { return wm * 64 + (i >> 2) * 32 + lm * 4 + (i & 3); }
-__device__ __forceinline__ int b_col(int wn, int ln, int j) { return wn * 32 + (j >> 2) * 16 + ln * 4 + (j & 3); }
-
-// a[k][i] = A(a_row(i), 4*kq + k) from an MN-major [BK][BM] tile.
-__device__ __forceinline__ void load_a(const float *sa, int kq, int wm, int lm, float (&a)[4][8]) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const float *row = sa + (kq * 4 + k) * BM + wm * 64 + lm * 4;
-        const float4 v0 = *reinterpret_cast<const float4 *>(row);
-        const float4 v1 = *reinterpret_cast<const float4 *>(row + 32);
-        a[k][0] = v0.x; a[k][1] = v0.y; a[k][2] = v0.z; a[k][3] = v0.w;
-        a[k][4] = v1.x; a[k][5] = v1.y; a[k][6] = v1.z; a[k][7] = v1.w;
-    }
+template <int JN>
+__device__ __forceinline__ int b_col(int wn, int ln, int j) {
+    return wn * (8 * JN) + (j >> 2) * 16 + ln * 4 + (j & 3);
 }
 
-// b[k][j] = B(4*kq + k, b_col(j)) from an MN-major [BK][BN] tile.
-__device__ __forceinline__ void load_b(const float *sb, int kq, int wn, int ln, float (&b)[4][8]) {
+// a[i] = A(a_row(i), k) from an MN-major [BK][BM] tile.
+__device__ __forceinline__ void load_a(const float *sa, int k, int wm, int lm, float (&a)[8]) {
+    const float *row = sa + k * BM + wm * 64 + lm * 4;
+    const float4 v0 = *reinterpret_cast<const float4 *>(row);
+    const float4 v1 = *reinterpret_cast<const float4 *>(row + 32);
+    a[0] = v0.x; a[1] = v0.y; a[2] = v0.z; a[3] = v0.w;
+    a[4] = v1.x; a[5] = v1.y; a[6] = v1.z; a[7] = v1.w;
+}
+
+// b[j] = B(k, b_col(j)) from an MN-major [BK][BN] tile.
+template <int JN, int BN>
+__device__ __forceinline__ void load_b(const float *sb, int k, int wn, int ln, float (&b)[2 * JN]) {
+    const float *row = sb + k * BN + wn * (8 * JN) + ln * 4;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const float *row = sb + (kq * 4 + k) * BN + wn * 32 + ln * 4;
-        const float4 v0 = *reinterpret_cast<const float4 *>(row);
-        const float4 v1 = *reinterpret_cast<const float4 *>(row + 16);
-        b[k][0] = v0.x; b[k][1] = v0.y; b[k][2] = v0.z; b[k][3] = v0.w;
-        b[k][4] = v1.x; b[k][5] = v1.y; b[k][6] = v1.z; b[k][7] = v1.w;
+    for (int g = 0; g < JN / 2; ++g) {
+        const float4 v = *reinterpret_cast<const float4 *>(row + 16 * g);
+        b[4 * g] = v.x; b[4 * g + 1] = v.y; b[4 * g + 2] = v.z; b[4 * g + 3] = v.w;
     }
 }
 
@@ -147,8 +152,9 @@ __device__ __forceinline__ void load_b(const float *sb, int kq, int wn, int ln, 
 // line-groups (lane = chunk + 4 * group), so both the four LDS.128 (8 distinct
 // swizzled chunks per 128 B row pair) and the four STS.128 (8 distinct groups
 // per k row) move 512 B in 4 wavefronts, the minimum.
+template <int LINES>
 __device__ __forceinline__ void transpose_tile(const float *src, float *dst, int xw, int lane) {
-    for (int it = xw; it < 8; it += XWARPS) {
+    for (int it = xw; it < LINES / 16; it += XWARPS) {
         const int c = (it & 1) * 4 + (lane & 3);
         const int g = (it >> 1) * 8 + (lane >> 2);
         float4 r[4];
@@ -157,19 +163,20 @@ __device__ __forceinline__ void transpose_tile(const float *src, float *dst, int
             const int line = 4 * g + q;
             r[q] = *reinterpret_cast<const float4 *>(src + line * KSUB + ((c ^ (line & 7)) << 2));
         }
-        float *d = dst + (4 * c) * 128 + 4 * g;
-        *reinterpret_cast<float4 *>(d + 0 * 128) = make_float4(r[0].x, r[1].x, r[2].x, r[3].x);
-        *reinterpret_cast<float4 *>(d + 1 * 128) = make_float4(r[0].y, r[1].y, r[2].y, r[3].y);
-        *reinterpret_cast<float4 *>(d + 2 * 128) = make_float4(r[0].z, r[1].z, r[2].z, r[3].z);
-        *reinterpret_cast<float4 *>(d + 3 * 128) = make_float4(r[0].w, r[1].w, r[2].w, r[3].w);
+        float *d = dst + (4 * c) * LINES + 4 * g;
+        *reinterpret_cast<float4 *>(d + 0 * LINES) = make_float4(r[0].x, r[1].x, r[2].x, r[3].x);
+        *reinterpret_cast<float4 *>(d + 1 * LINES) = make_float4(r[0].y, r[1].y, r[2].y, r[3].y);
+        *reinterpret_cast<float4 *>(d + 2 * LINES) = make_float4(r[0].z, r[1].z, r[2].z, r[3].z);
+        *reinterpret_cast<float4 *>(d + 3 * LINES) = make_float4(r[0].w, r[1].w, r[2].w, r[3].w);
     }
 }
 
-template <bool AK, bool BKM>
-__global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
+template <bool AK, bool BKM, int BN>
+__global__ void __launch_bounds__(Geo<AK, BKM, BN>::THREADS, 1)
     gemm_ffma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const Params p) {
-    using G = Geo<AK, BKM>;
+    using G = Geo<AK, BKM, BN>;
+    constexpr int JN = G::JN;
     constexpr int STAGES = G::STAGES, A_TILE = G::A_TILE, B_TILE = G::B_TILE, SF = G::STAGE_FLOATS;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzled K-major tiles
@@ -232,8 +239,8 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
                 unit_range(u, p, t, kb0, kb1);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
-                    if constexpr (G::XA) transpose_tile(raw_a(stage), x_a(stage), xw, lane);
-                    if constexpr (G::XB) transpose_tile(raw_b(stage), x_b(stage), xw, lane);
+                    if constexpr (G::XA) transpose_tile<BM>(raw_a(stage), x_a(stage), xw, lane);
+                    if constexpr (G::XB) transpose_tile<BN>(raw_b(stage), x_b(stage), xw, lane);
                     mbar_arrive(&xfull[stage]);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[stage]);
@@ -257,11 +264,11 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
         tile_coords(t, p, tm, tn);
         // acc2[i][jp] = (acc(i, 2jp), acc(i, 2jp+1)): pairs along n, where one
         // LDS.128 of the MN-major B tile delivers adjacent columns
-        unsigned long long acc2[8][4];
+        unsigned long long acc2[8][JN];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
+            for (int j = 0; j < JN; ++j) acc2[i][j] = 0ull;
 
         for (int kb = kb0; kb < kb1; ++kb) {
             if constexpr (!(G::XA && G::XB)) mbar_wait(&full[stage], phase);   // reads a raw tile
@@ -269,20 +276,17 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
             const float *sa = G::XA ? x_a(stage) : raw_a(stage);
             const float *sb = G::XB ? x_b(stage) : raw_b(stage);
 #pragma unroll
-            for (int kq = 0; kq < BK / 4; ++kq) {
-                float a[4][8], b[4][8];
-                load_a(sa, kq, wm, lm, a);
-                load_b(sb, kq, wn, ln, b);
+            for (int k = 0; k < BK; ++k) {
+                float a[8], b[2 * JN];
+                load_a(sa, k, wm, lm, a);
+                load_b<JN, BN>(sb, k, wn, ln, b);
+                unsigned long long bp[JN];   // adjacent registers: packing is free
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    unsigned long long bp[4];   // adjacent registers: packing is free
+                for (int jp = 0; jp < JN; ++jp) bp[jp] = pack2(b[2 * jp], b[2 * jp + 1]);
 #pragma unroll
-                    for (int jp = 0; jp < 4; ++jp) bp[jp] = pack2(b[k][2 * jp], b[k][2 * jp + 1]);
+                for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
-#pragma unroll
-                        for (int jp = 0; jp < 4; ++jp) ffma2(acc2[i][jp], a[k][i], bp[jp]);
-                }
+                    for (int jp = 0; jp < JN; ++jp) ffma2(acc2[i][jp], a[i], bp[jp]);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
@@ -296,15 +300,17 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
             // partials in slice order -- a fixed order, so the result does not
             // depend on which slice finishes first -- and stores C.
             const int ctid = threadIdx.x;   // 0 .. CWARPS*32-1
-            float4 *mine = reinterpret_cast<float4 *>(p.ws + int64_t(u) * (BM * BN)) + ctid * 16;
+            constexpr int PER = 8 * JN / 2;   // float4 per thread
+            float4 *mine = reinterpret_cast<float4 *>(p.ws + int64_t(u) * (BM * BN)) + ctid * PER;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                float lo0, hi0, lo1, hi1, lo2, hi2, lo3, hi3;
-                unpack2(acc2[i][0], lo0, hi0); unpack2(acc2[i][1], lo1, hi1);
-                unpack2(acc2[i][2], lo2, hi2); unpack2(acc2[i][3], lo3, hi3);
-                __stcg(mine + 2 * i, make_float4(lo0, hi0, lo1, hi1));
-                __stcg(mine + 2 * i + 1, make_float4(lo2, hi2, lo3, hi3));
-            }
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int jp = 0; jp < JN; jp += 2) {
+                    float lo0, hi0, lo1, hi1;
+                    unpack2(acc2[i][jp], lo0, hi0);
+                    unpack2(acc2[i][jp + 1], lo1, hi1);
+                    __stcg(mine + (i * JN + jp) / 2, make_float4(lo0, hi0, lo1, hi1));
+                }
             __threadfence();
             named_bar_sync(1, CWARPS * 32);
             if (ctid == 0) last_flag = (atomicAdd(p.sem + t, 1) == p.splits - 1);
@@ -312,19 +318,21 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
             const bool last = last_flag;
             if (!last) continue;
             __threadfence();
-            const float4 *base = reinterpret_cast<const float4 *>(p.ws + int64_t(t) * p.splits * (BM * BN)) + ctid * 16;
+            const float4 *base =
+                reinterpret_cast<const float4 *>(p.ws + int64_t(t) * p.splits * (BM * BN)) + ctid * PER;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                float4 s0 = __ldcg(base + 2 * i), s1 = __ldcg(base + 2 * i + 1);
-                for (int sl = 1; sl < p.splits; ++sl) {
-                    const float4 q0 = __ldcg(base + sl * (BM * BN / 4) + 2 * i);
-                    const float4 q1 = __ldcg(base + sl * (BM * BN / 4) + 2 * i + 1);
-                    s0.x += q0.x; s0.y += q0.y; s0.z += q0.z; s0.w += q0.w;
-                    s1.x += q1.x; s1.y += q1.y; s1.z += q1.z; s1.w += q1.w;
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int jp = 0; jp < JN; jp += 2) {
+                    float4 s0 = __ldcg(base + (i * JN + jp) / 2);
+#pragma unroll 1
+                    for (int sl = 1; sl < p.splits; ++sl) {
+                        const float4 q0 = __ldcg(base + sl * (BM * BN / 4) + (i * JN + jp) / 2);
+                        s0.x += q0.x; s0.y += q0.y; s0.z += q0.z; s0.w += q0.w;
+                    }
+                    acc2[i][jp] = pack2(s0.x, s0.y);
+                    acc2[i][jp + 1] = pack2(s0.z, s0.w);
                 }
-                acc2[i][0] = pack2(s0.x, s0.y); acc2[i][1] = pack2(s0.z, s0.w);
-                acc2[i][2] = pack2(s1.x, s1.y); acc2[i][3] = pack2(s1.z, s1.w);
-            }
             if (ctid == 0) p.sem[t] = 0;   // ready for the next launch
         }
 
@@ -334,13 +342,13 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
         for (int i = 0; i < 8; ++i) {
             const int row = m0 + a_row(wm, lm, i);
             if (row >= p.M) continue;
-            float acc[8];
+            float acc[2 * JN];
 #pragma unroll
-            for (int jp = 0; jp < 4; ++jp) unpack2(acc2[i][jp], acc[2 * jp], acc[2 * jp + 1]);
+            for (int jp = 0; jp < JN; ++jp) unpack2(acc2[i][jp], acc[2 * jp], acc[2 * jp + 1]);
             float *crow = p.C + int64_t(row) * p.ldc;
 #pragma unroll
-            for (int jq = 0; jq < 2; ++jq) {
-                const int col = n0 + b_col(wn, ln, jq * 4);
+            for (int jq = 0; jq < JN / 2; ++jq) {
+                const int col = n0 + b_col<JN>(wn, ln, jq * 4);
                 if (p.c_vec && col + 3 < p.N) {
                     *reinterpret_cast<float4 *>(crow + col) =
                         make_float4(acc[jq * 4 + 0], acc[jq * 4 + 1], acc[jq * 4 + 2], acc[jq * 4 + 3]);
@@ -354,9 +362,10 @@ __global__ void __launch_bounds__(Geo<AK, BKM>::THREADS, 1)
     }
 }
 
-template <bool AK, bool BKM>
+template <bool AK, bool BKM, int BN>
 static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
-    using G = Geo<AK, BKM>;
+    using G = Geo<AK, BKM, BN>;
+    static_assert(G::STAGES >= 2, "stage ring does not fit");
     CUtensorMap ta, tb;
     cudaError_t e;
     if (AK) e = make_tmap_2d(&ta, p.A, p.K, p.M, p.lda, KSUB, BM, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -396,7 +405,7 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
         if (e != cudaSuccess) { cudaFreeAsync(buf, s); return e; }
     }
 
-    auto kern = gemm_ffma_kernel<AK, BKM>;
+    auto kern = gemm_ffma_kernel<AK, BKM, BN>;
     static bool attr_done = false;  // benign race: setting the attribute twice is harmless
     if (!attr_done) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::SMEM_BYTES));
@@ -432,10 +441,26 @@ cudaError_t launch_ffma(const Problem &p, const Knobs &kn, cudaStream_t s) {
     using namespace ffma;
     const bool AK = (p.la == 0);   // row-major A: K contiguous
     const bool BKM = (p.lb == 1);  // column-major B: K contiguous
-    if (AK && BKM)  return launch_t<true, true>(p, kn, s);
-    if (AK && !BKM) return launch_t<true, false>(p, kn, s);
-    if (!AK && BKM) return launch_t<false, true>(p, kn, s);
-    return launch_t<false, false>(p, kn, s);
+    // Tile width: 128 x 256 tiles (8 x 16 per thread: 6 LDS.128 per 64 FFMA2)
+    // run 2-5% faster per flop than 128 x 128 (8 x 8: 4 per 32) at n = 8192
+    // (profiles/r01_ab_ffma_bn256.txt) but halve the tile count, so take 256
+    // unless 128 fills the persistent grid's waves better by more than that.
+    const int grid = kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms;
+    auto eff = [&](int bn, double kern) {
+        const int64_t tiles = int64_t((p.M + BM - 1) / BM) * ((p.N + bn - 1) / bn);
+        const int64_t waves = (tiles + grid - 1) / grid;
+        return kern * double(tiles) / double(waves * grid) * double(p.N) / double(((p.N + bn - 1) / bn) * bn);
+    };
+    if (eff(256, 1.04) >= eff(128, 1.0)) {
+        if (AK && BKM)  return launch_t<true, true, 256>(p, kn, s);
+        if (AK && !BKM) return launch_t<true, false, 256>(p, kn, s);
+        if (!AK && BKM) return launch_t<false, true, 256>(p, kn, s);
+        return launch_t<false, false, 256>(p, kn, s);
+    }
+    if (AK && BKM)  return launch_t<true, true, 128>(p, kn, s);
+    if (AK && !BKM) return launch_t<true, false, 128>(p, kn, s);
+    if (!AK && BKM) return launch_t<false, true, 128>(p, kn, s);
+    return launch_t<false, false, 128>(p, kn, s);
 }
 
 }  // namespace lpy
