@@ -306,12 +306,18 @@ lpy_status lpy_gemm_f32_host(int64_t M, int64_t N, int64_t K, const float *A, in
     // panel, the panel products as their inputs land, and D2H of each C panel
     // as soon as it is computed -- so the C download and the products hide
     // under the A upload (PCIe is full duplex).  Panels are multiples of 128
-    // rows (the output tile), at most 8 of them.
-    const int64_t prow = M <= 1024 ? M : ((M + 7) / 8 + 127) / 128 * 128;
+    // rows (the output tile).  At n = 8192 the call is upload-bound: 537 MB at
+    // the measured 53 GB/s (47.5 each way while the C download runs) is
+    // ~10.7 ms of the ~11.8 ms measured; 16 vs 8 panels measured equal.
+    constexpr int kMaxPanels = 16;
+    // panels of >= 512 rows (multiples of 128), at most kMaxPanels: the last
+    // panel's product and download are the exposed tail after the upload ends
+    const int64_t prow = M <= 1024 ? M
+                                   : std::max<int64_t>(512, ((M + kMaxPanels - 1) / kMaxPanels + 127) / 128 * 128);
     const int npanel = int((M + prow - 1) / prow);
     cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_b = nullptr, ev_done = nullptr;
-    cudaEvent_t ev_a[8] = {}, ev_c[8] = {};
+    cudaEvent_t ev_a[kMaxPanels] = {}, ev_c[kMaxPanels] = {};
     auto mk_stream = [&](cudaStream_t *x) {
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(x, cudaStreamNonBlocking);
     };
