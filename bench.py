@@ -221,18 +221,20 @@ def run_reference(args, rank, world):
 
 
 # --------------------------------------------------------------------------- GPU arm
-def make_inputs(n, rank, world, chunks, device):
-    """This rank's A panel and (on rank 0) B in column-blocked storage."""
+def make_inputs(n, rank, world, chunks, device, owners=False, comm_world=None):
+    """This rank's A panel and the column blocks of B it holds before the step
+    (all of them on rank 0, or block c on rank c mod world with owners=True)."""
     import numpy as np
     import torch
     import synth
-    from paper_1405_7470_b200.dist import chunk_bounds, panel_bounds
+    from paper_1405_7470_b200.dist import block_owner, chunk_bounds, panel_bounds
     r0, r1 = panel_bounds(n, world, rank)
     A = torch.from_numpy(synth.matrix(r1 - r0, n, seed=0, matrix_id=synth.MATRIX_A, row0=r0)).to(device)
     bounds = chunk_bounds(n, chunks)
     blocks = []
-    for c0, c1 in bounds:
-        if rank == 0:
+    cw = comm_world or world
+    for c, (c0, c1) in enumerate(bounds):
+        if rank == block_owner(c, cw, 0, owners):
             blk = synth.matrix(n, c1 - c0, seed=0, matrix_id=synth.MATRIX_B, col0=c0)
             blocks.append(torch.from_numpy(blk).to(device))
         else:
@@ -250,7 +252,8 @@ def time_path(args, path, rank, world, device, dist_on):
     r0_, r1_ = panel_bounds(n, pw, rank)
     sms = torch.cuda.get_device_properties(device).multi_processor_count
     chunks = (args.chunks or choose_chunks(r1_ - r0_, n, sms)) if dist_on else 1
-    A, blocks, C, bounds, (r0, r1) = make_inputs(n, rank, pw, chunks, device)
+    owners = args.bcast == "owners"
+    A, blocks, C, bounds, (r0, r1) = make_inputs(n, rank, pw, chunks, device, owners, world)
 
     def gemm_fn(a, b, c):
         opts = None
@@ -266,7 +269,8 @@ def time_path(args, path, rank, world, device, dist_on):
         if not dist_on:
             lpy.gemm(A, blocks[0], out=C, path=path)
         else:
-            rowpanel_gemm(A, blocks, C, bounds, gemm_fn=gemm_fn, comm_stream=comm, compute_streams=cstreams)
+            rowpanel_gemm(A, blocks, C, bounds, gemm_fn=gemm_fn, comm_stream=comm, compute_streams=cstreams,
+                          owners=owners)
 
     for _ in range(args.warmup):
         step()
@@ -313,7 +317,9 @@ def time_path(args, path, rank, world, device, dist_on):
         reps = max(3, min(args.steps, 10))
         # the two halves of a step, each timed alone (max over ranks): B's broadcast
         # (4*K*N bytes from rank 0) and this rank's panel products
-        bcast_ms = timed(lambda: [dist.broadcast(b, src=0) for b in blocks], reps)
+        from paper_1405_7470_b200.dist import block_owner
+        bcast_ms = timed(lambda: [dist.broadcast(b, src=block_owner(c, world, 0, owners))
+                                  for c, b in enumerate(blocks)], reps)
         gemm_ms = timed(lambda: rowpanel_gemm(A, blocks, C, bounds, gemm_fn=gemm_fn, comm_stream=comm,
                                               compute_streams=cstreams, broadcast=False), reps)
         nbytes = 4 * n * n
@@ -545,6 +551,9 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "ffma", "3xtf32"])
     ap.add_argument("--also", default="ffma", help="secondary path to report ('' for none)")
     ap.add_argument("--chunks", type=int, default=0, help="B column blocks for N>1 (0 = ~1 wave each)")
+    ap.add_argument("--bcast", default="root", choices=["root", "owners"],
+                    help="N>1: B starts on rank 0 and is broadcast (north_star), or starts sharded by "
+                         "column blocks and each owner broadcasts its blocks")
     ap.add_argument("--emulate-ranks", type=int, default=0,
                     help="diagnostics at N=1 with --force-dist: rank 0's panel of an N-rank split (not a bench value)")
     ap.add_argument("--force-dist", action="store_true",
@@ -629,7 +638,7 @@ def main():
             "data": "synthetic: seeded SplitMix64 uniform[-1,1) fp32 on a 2^-23 grid",
             "config": {"workload": f"n={n} square fp32 C=A*B, row-major A/B/C (BASELINE config 4)",
                        "path": res["path"], "M": n, "N": n, "K": n,
-                       "parallelism": f"rowpanel{world}" + (f"+nccl_bcast_B_chunks{res['chunks']}" if dist_on else ""),
+                       "parallelism": f"rowpanel{world}" + (f"+nccl_bcast_B_chunks{res['chunks']}" + ("_owners" if args.bcast == "owners" else "") if dist_on else ""),
                        "l2": "inputs larger than L2 (A, B, C 268 MB each > 126 MB), no flush"},
             "roofline": roof(res, res["path"]),
             "cpu_baseline": cpu,

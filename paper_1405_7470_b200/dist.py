@@ -77,13 +77,24 @@ def chunk_grid(rows: int, cols: int, sms: int, path: str) -> int:
     return max(1, min(sms, math.ceil(rows / 128) * math.ceil(cols / 128)))
 
 
+def block_owner(c: int, world: int, root: int = 0, owners: bool = False) -> int:
+    """Rank holding column block c of B before the step: `root` for the
+    north_star's broadcast of B, or rank c mod world when B starts sharded
+    by column blocks (`owners=True`: every rank broadcasts the blocks it holds,
+    so the send load -- and B's generation -- is spread over all ranks; an
+    all-gather of the blocks expressed as per-block broadcasts, since NCCL's
+    all-gather needs equal contiguous pieces and the blocks are column blocks)."""
+    return c % world if owners else root
+
+
 def rowpanel_gemm(A_panel, B_blocks, C_panel, bounds, group=None, root=0, gemm_fn=None,
-                  comm_stream=None, compute_streams=None, broadcast=True):
+                  comm_stream=None, compute_streams=None, broadcast=True, owners=False):
     """One distributed product step on this rank.
 
     A_panel : (rows_r, K) tensor, this rank's rows of A.
-    B_blocks: list of (K, w_c) contiguous tensors, the column blocks of B; valid
-              on `root`, receive buffers elsewhere.  Broadcast in order.
+    B_blocks: list of (K, w_c) contiguous tensors, the column blocks of B; block
+              c valid on block_owner(c) (root, or c mod world with owners=True),
+              receive buffers elsewhere.  Broadcast in order.
     C_panel : (rows_r, N) row-major tensor; column block c is written by
               gemm_fn(A_panel, B_blocks[c], C_panel[:, c0:c1]).
     bounds  : chunk_bounds(N, len(B_blocks)).
@@ -99,11 +110,13 @@ def rowpanel_gemm(A_panel, B_blocks, C_panel, bounds, group=None, root=0, gemm_f
 
         def gemm_fn(a, b, c):
             gemm_fn_default(a, b, out=c)
+    world = dist.get_world_size(group) if broadcast else 1
+    src = [block_owner(c, world, root, owners) for c in range(len(B_blocks))]
     if not A_panel.is_cuda:
         # CPU (gloo) path: same order, no overlap
-        for (c0, c1), blk in zip(bounds, B_blocks):
+        for c, ((c0, c1), blk) in enumerate(zip(bounds, B_blocks)):
             if broadcast:
-                dist.broadcast(blk, src=root, group=group)
+                dist.broadcast(blk, src=src[c], group=group)
             gemm_fn(A_panel, blk, C_panel[:, c0:c1])
         return None
 
@@ -115,10 +128,10 @@ def rowpanel_gemm(A_panel, B_blocks, C_panel, bounds, group=None, root=0, gemm_f
     for st in streams:
         st.wait_stream(caller)
     events = []
-    for blk in B_blocks:
+    for c, blk in enumerate(B_blocks):
         if broadcast:
             with torch.cuda.stream(comm):
-                dist.broadcast(blk, src=root, group=group)
+                dist.broadcast(blk, src=src[c], group=group)
         ev = torch.cuda.Event()
         ev.record(comm)
         events.append(ev)

@@ -13,8 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1405_7470_b200.dist import (chunk_bounds, chunk_grid, chunk_streams, choose_chunks, panel_bounds,
-                                       rowpanel_gemm)
+from paper_1405_7470_b200.dist import (block_owner, chunk_bounds, chunk_grid, chunk_streams, choose_chunks,
+                                       panel_bounds, rowpanel_gemm)
 
 
 def test_panel_bounds_cover_rows_exactly():
@@ -61,7 +61,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, M, N, K, chunks, q):
+def _worker(rank, world, port, M, N, K, chunks, q, owners=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -72,8 +72,8 @@ def _worker(rank, world, port, M, N, K, chunks, q):
         A = torch.from_numpy(synth.matrix(r1 - r0, K, seed=3, matrix_id=0, row0=r0))
         bounds = chunk_bounds(N, chunks)
         blocks = []
-        for c0, c1 in bounds:
-            if rank == 0:
+        for c, (c0, c1) in enumerate(bounds):
+            if rank == block_owner(c, world, 0, owners):
                 blocks.append(torch.from_numpy(synth.matrix(K, c1 - c0, seed=3, matrix_id=1, col0=c0)))
             else:
                 blocks.append(torch.full((K, c1 - c0), float("nan")))
@@ -86,7 +86,7 @@ def _worker(rank, world, port, M, N, K, chunks, q):
                                  b.contiguous().numpy().reshape(-1), n, 0)
             c.copy_(torch.from_numpy(ref.astype(np.float32)))
 
-        rowpanel_gemm(A, blocks, C, bounds, gemm_fn=gemm_fn)
+        rowpanel_gemm(A, blocks, C, bounds, gemm_fn=gemm_fn, owners=owners)
         # every rank now holds all of B (the broadcast), and its panel of C
         B_full = torch.cat(blocks, dim=1)
         if rank == 0:
@@ -100,15 +100,16 @@ def _worker(rank, world, port, M, N, K, chunks, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,M,N,K,chunks", [(2, 256, 384, 96, 3), (3, 200, 300, 64, 2),
-                                                (2, 130, 128, 33, 1)])
-def test_rowpanel_gloo(world, M, N, K, chunks):
+@pytest.mark.parametrize("world,M,N,K,chunks,owners", [(2, 256, 384, 96, 3, False), (3, 200, 300, 64, 2, False),
+                                                       (2, 130, 128, 33, 1, False), (3, 256, 768, 40, 3, True),
+                                                       (2, 300, 1024, 24, 4, True)])
+def test_rowpanel_gloo(world, M, N, K, chunks, owners):
     import oracle
     import synth
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, M, N, K, chunks, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, M, N, K, chunks, q, owners)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=120) for _ in range(world)]
