@@ -174,6 +174,15 @@ def _stream_handle(stream):
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
+def _one_device(*tensors):
+    """The single CUDA device all `tensors` live on (the C ABI works on the
+    current device, so calls run under a guard for it); raises otherwise."""
+    devs = {t.device for t in tensors}
+    if len(devs) != 1 or next(iter(devs)).type != "cuda":
+        raise ValueError(f"all operands must be on one CUDA device, got {sorted(map(str, devs))}")
+    return next(iter(devs))
+
+
 def _path_id(path) -> int:
     return PATHS[path] if isinstance(path, str) else int(path)
 
@@ -205,8 +214,9 @@ def gemm(A, B, out=None, path="auto", stream=None, opts: GemmOpts | None = None)
     lc = operand_layout(out)
     if lc is None:
         raise ValueError("out must be row- or column-major")
-    st = lpy_gemm_f32_ex(M, N, K, A.data_ptr(), la[1], la[0], B.data_ptr(), lb[1], lb[0],
-                         out.data_ptr(), lc[1], lc[0], _stream_handle(stream), _path_id(path), opts)
+    with torch.cuda.device(_one_device(A, B, out)):
+        st = lpy_gemm_f32_ex(M, N, K, A.data_ptr(), la[1], la[0], B.data_ptr(), lb[1], lb[0],
+                             out.data_ptr(), lc[1], lc[0], _stream_handle(stream), _path_id(path), opts)
     if st != 0:
         raise LpyError(st, "lpy_gemm_f32_ex")
     return out
@@ -243,9 +253,11 @@ def saxpy(alpha, x, y, stream=None):
         raise ValueError("x and y must have the same length")
     if not (x.is_cuda and y.is_cuda):
         raise ValueError("device tensors required (use saxpy_host for host buffers)")
+    import torch
     incx, incy = _vec(x, "x"), _vec(y, "y")
-    st = lpy_saxpy_f32(x.shape[0], float(alpha), x.data_ptr(), incx, y.data_ptr(), incy,
-                       _stream_handle(stream))
+    with torch.cuda.device(_one_device(x, y)):
+        st = lpy_saxpy_f32(x.shape[0], float(alpha), x.data_ptr(), incx, y.data_ptr(), incy,
+                           _stream_handle(stream))
     if st != 0:
         raise LpyError(st, "lpy_saxpy_f32")
     return y
@@ -284,8 +296,9 @@ def coulomb(targets, sources, charges, out=None, stream=None):
     nt = targets.shape[0]
     if out is None:
         out = torch.empty(nt, dtype=torch.float32, device=targets.device)
-    st = lpy_coulomb_f32(nt, targets.data_ptr(), ldt, sources.shape[0], sources.data_ptr(), lds,
-                         charges.data_ptr(), out.data_ptr(), _stream_handle(stream))
+    with torch.cuda.device(_one_device(targets, sources, charges, out)):
+        st = lpy_coulomb_f32(nt, targets.data_ptr(), ldt, sources.shape[0], sources.data_ptr(), lds,
+                             charges.data_ptr(), out.data_ptr(), _stream_handle(stream))
     if st != 0:
         raise LpyError(st, "lpy_coulomb_f32")
     return out
