@@ -561,11 +561,13 @@ cudaError_t launch_3xtf32(const Problem &p, const Knobs &kn, cudaStream_t s) {
         const char *e = getenv("LPY_TF32_BN");
         return e ? atoi(e) : 0;
     }();
-    // the tile width follows the grid the caller gives (opts.num_ctas), so a
-    // product sharing the GPU with others (dist.py's per-chunk products) keeps
-    // full-width tiles; per-element sums do not depend on the width
-    const int pairs = (kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms) / 2;
-    switch (force_bn ? force_bn : tf32::choose_bn(p.M, p.N, pairs > 0 ? pairs : 1)) {
+    // the tile width comes from the shape and the device (the tail split
+    // follows the tile count, and results must not depend on opts.num_ctas),
+    // or from opts.tile_n (dist.py's per-chunk products, which share the GPU,
+    // ask for full-width tiles)
+    const int pairs = kn.num_sms / 2;
+    const int bn = kn.tile_n ? kn.tile_n : force_bn ? force_bn : tf32::choose_bn(p.M, p.N, pairs > 0 ? pairs : 1);
+    switch (bn) {
         case 128: return tf32::launch_cg<2, 128>(p, kn, s);
         case 192: return tf32::launch_cg<2, 192>(p, kn, s);
         default:  return tf32::launch_cg<2, 256>(p, kn, s);

@@ -48,7 +48,7 @@ constexpr int XWARPS = 3;                    // transpose warps (warps CWARPS+1 
 // Per-layout geometry.  AK: A is K-major (row-major A); BKM: B is K-major
 // (column-major B).  Each stage holds the raw TMA tiles plus MN-major copies
 // of the K-major ones.
-template <bool AK, bool BKM, int BN>
+template <bool AK, bool BKM, int BN, bool SPLIT = false>
 struct Geo {
     static constexpr bool XA = AK, XB = BKM, X = AK || BKM;
     static constexpr int JN = BN / 32;                     // column pairs per thread (8 x 2JN micro-tile)
@@ -78,7 +78,6 @@ struct Params {
     // u = tile * splits + slice covers k-blocks [slice*KB/splits, (slice+1)*KB/splits)
     int splits, num_units;
     float *ws;       // [num_units][BM*BN] partial tiles (splits > 1)
-    int *sem;        // [num_tiles] arrival counters, zero on entry, left zero on exit
 };
 
 __device__ __forceinline__ void unit_range(int u, const Params &p, int &t, int &kb0, int &kb1) {
@@ -171,11 +170,11 @@ __device__ __forceinline__ void transpose_tile(const float *src, float *dst, int
     }
 }
 
-template <bool AK, bool BKM, int BN>
-__global__ void __launch_bounds__(Geo<AK, BKM, BN>::THREADS, 1)
+template <bool AK, bool BKM, int BN, bool SPLIT>
+__global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
     gemm_ffma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const Params p) {
-    using G = Geo<AK, BKM, BN>;
+    using G = Geo<AK, BKM, BN, SPLIT>;
     constexpr int JN = G::JN;
     constexpr int STAGES = G::STAGES, A_TILE = G::A_TILE, B_TILE = G::B_TILE, SF = G::STAGE_FLOATS;
     extern __shared__ uint8_t smem_raw[];
@@ -241,6 +240,9 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN>::THREADS, 1)
                     mbar_wait(&full[stage], phase);
                     if constexpr (G::XA) transpose_tile<BM>(raw_a(stage), x_a(stage), xw, lane);
                     if constexpr (G::XB) transpose_tile<BN>(raw_b(stage), x_b(stage), xw, lane);
+                    // this lane's STS of the copy (and LDS of the raw tile) must be
+                    // complete before it publishes the copy and frees the raw tile
+                    asm volatile("fence.acq_rel.cta;" ::: "memory");
                     mbar_arrive(&xfull[stage]);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[stage]);
@@ -257,7 +259,6 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN>::THREADS, 1)
     const int lm = lane >> 2, ln = lane & 3;
     int stage = 0;
     uint32_t phase = 0;
-    __shared__ int last_flag;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
         int t, kb0, kb1, tm, tn;
         unit_range(u, p, t, kb0, kb1);
@@ -288,20 +289,18 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN>::THREADS, 1)
 #pragma unroll
                     for (int jp = 0; jp < JN; ++jp) ffma2(acc2[i][jp], a[i], bp[jp]);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
+            mbar_arrive_after_reads(&empty[stage], lane);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
 
-        if (p.splits > 1) {
-            // ---------------------------------------- split-K fix-up
-            // Every slice parks its partial tile in the workspace (each thread its
-            // own 64 floats, contiguous); the slice that arrives last sums all
-            // partials in slice order -- a fixed order, so the result does not
-            // depend on which slice finishes first -- and stores C.
-            const int ctid = threadIdx.x;   // 0 .. CWARPS*32-1
+        if constexpr (SPLIT) {
+            // ---------------------------------------- split-K: park the partial
+            // Every slice stores its partial tile (each thread its own 8 x 2JN
+            // values, contiguous) and the fix-up kernel (splitk_fixup) adds the
+            // slices of each tile in slice order -- a fixed order, independent of
+            // which slice finished first.
             constexpr int PER = 8 * JN / 2;   // float4 per thread
-            float4 *mine = reinterpret_cast<float4 *>(p.ws + int64_t(u) * (BM * BN)) + ctid * PER;
+            float4 *mine = reinterpret_cast<float4 *>(p.ws + int64_t(u) * (BM * BN)) + threadIdx.x * PER;
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -309,31 +308,9 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN>::THREADS, 1)
                     float lo0, hi0, lo1, hi1;
                     unpack2(acc2[i][jp], lo0, hi0);
                     unpack2(acc2[i][jp + 1], lo1, hi1);
-                    __stcg(mine + (i * JN + jp) / 2, make_float4(lo0, hi0, lo1, hi1));
+                    mine[(i * JN + jp) / 2] = make_float4(lo0, hi0, lo1, hi1);
                 }
-            __threadfence();
-            named_bar_sync(1, CWARPS * 32);
-            if (ctid == 0) last_flag = (atomicAdd(p.sem + t, 1) == p.splits - 1);
-            named_bar_sync(1, CWARPS * 32);
-            const bool last = last_flag;
-            if (!last) continue;
-            __threadfence();
-            const float4 *base =
-                reinterpret_cast<const float4 *>(p.ws + int64_t(t) * p.splits * (BM * BN)) + ctid * PER;
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                for (int jp = 0; jp < JN; jp += 2) {
-                    float4 s0 = __ldcg(base + (i * JN + jp) / 2);
-#pragma unroll 1
-                    for (int sl = 1; sl < p.splits; ++sl) {
-                        const float4 q0 = __ldcg(base + sl * (BM * BN / 4) + (i * JN + jp) / 2);
-                        s0.x += q0.x; s0.y += q0.y; s0.z += q0.z; s0.w += q0.w;
-                    }
-                    acc2[i][jp] = pack2(s0.x, s0.y);
-                    acc2[i][jp + 1] = pack2(s0.z, s0.w);
-                }
-            if (ctid == 0) p.sem[t] = 0;   // ready for the next launch
+            continue;
         }
 
         // ------------------------------------------------ epilogue (ragged-edge stores)
@@ -357,6 +334,51 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN>::THREADS, 1)
                     for (int e = 0; e < 4; ++e)
                         if (col + e < p.N) crow[col + e] = acc[jq * 4 + e];
                 }
+            }
+        }
+    }
+}
+
+// Split-K fix-up: one CTA of 256 threads per output tile; thread ctid owns the
+// elements consumer thread ctid of the GEMM kernel owned (same a_row / b_col
+// map), adds the tile's slice partials in slice order and stores C with the
+// same ragged-edge predicates.
+template <int BN>
+__global__ void __launch_bounds__(CWARPS * 32) splitk_fixup_kernel(const Params p) {
+    constexpr int JN = BN / 32, PER = 8 * JN / 2;
+    const int t = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = warp >> 2, wn = warp & 3, lm = lane >> 2, ln = lane & 3;
+    int tm, tn;
+    tile_coords(t, p, tm, tn);
+    const float4 *base = reinterpret_cast<const float4 *>(p.ws + int64_t(t) * p.splits * (BM * BN)) +
+                         threadIdx.x * PER;
+    const int m0 = tm * BM, n0 = tn * BN;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = m0 + a_row(wm, lm, i);
+        float acc[2 * JN];
+#pragma unroll
+        for (int h = 0; h < JN / 2; ++h) {
+            float4 s0 = base[i * (JN / 2) + h];
+            for (int sl = 1; sl < p.splits; ++sl) {
+                const float4 q = base[int64_t(sl) * (BM * BN / 4) + i * (JN / 2) + h];
+                s0.x += q.x; s0.y += q.y; s0.z += q.z; s0.w += q.w;
+            }
+            acc[4 * h] = s0.x; acc[4 * h + 1] = s0.y; acc[4 * h + 2] = s0.z; acc[4 * h + 3] = s0.w;
+        }
+        if (row >= p.M) continue;
+        float *crow = p.C + int64_t(row) * p.ldc;
+#pragma unroll
+        for (int jq = 0; jq < JN / 2; ++jq) {
+            const int col = n0 + b_col<JN>(wn, ln, jq * 4);
+            if (p.c_vec && col + 3 < p.N) {
+                *reinterpret_cast<float4 *>(crow + col) =
+                    make_float4(acc[jq * 4 + 0], acc[jq * 4 + 1], acc[jq * 4 + 2], acc[jq * 4 + 3]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (col + e < p.N) crow[col + e] = acc[jq * 4 + e];
             }
         }
     }
@@ -387,33 +409,31 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     prm.splits = choose_splits(prm.num_tiles, prm.k_blocks, kn.num_sms, 4, 8);
     prm.num_units = prm.num_tiles * prm.splits;
     prm.ws = nullptr;
-    prm.sem = nullptr;
     int grid = kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms;
     if (grid > prm.num_units) grid = prm.num_units;
     if (grid < 1) grid = 1;
     if (prm.splits > 1) {
         // The split is fixed by the shape and the device's SM count (never by
-        // opts.num_ctas), so results stay bitwise grid-invariant.  Scratch is
-        // stream-ordered: partial tiles, then the zeroed arrival counters.
+        // opts.num_ctas), so results stay bitwise grid-invariant.  Scratch
+        // (the partial tiles) is stream-ordered.
         const size_t ws_bytes = size_t(prm.num_units) * BM * BN * 4;
-        char *buf = nullptr;
-        e = cudaMallocAsync(reinterpret_cast<void **>(&buf), ws_bytes + size_t(prm.num_tiles) * 4, s);
+        e = cudaMallocAsync(reinterpret_cast<void **>(&prm.ws), ws_bytes, s);
         if (e != cudaSuccess) return e;
-        prm.ws = reinterpret_cast<float *>(buf);
-        prm.sem = reinterpret_cast<int *>(buf + ws_bytes);
-        e = cudaMemsetAsync(prm.sem, 0, size_t(prm.num_tiles) * 4, s);
-        if (e != cudaSuccess) { cudaFreeAsync(buf, s); return e; }
     }
 
-    auto kern = gemm_ffma_kernel<AK, BKM, BN>;
-    static bool attr_done = false;  // benign race: setting the attribute twice is harmless
-    if (!attr_done) {
+    auto kern = prm.splits > 1 ? gemm_ffma_kernel<AK, BKM, BN, true> : gemm_ffma_kernel<AK, BKM, BN, false>;
+    static bool attr_done[2] = {false, false};  // benign race: setting the attribute twice is harmless
+    if (!attr_done[prm.splits > 1]) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::SMEM_BYTES));
         if (e != cudaSuccess) return e;
-        attr_done = true;
+        attr_done[prm.splits > 1] = true;
     }
     kern<<<grid, G::THREADS, G::SMEM_BYTES, s>>>(ta, tb, prm);
     e = cudaGetLastError();
+    if (e == cudaSuccess && prm.splits > 1) {
+        splitk_fixup_kernel<BN><<<prm.num_tiles, CWARPS * 32, 0, s>>>(prm);
+        e = cudaGetLastError();
+    }
     if (prm.ws) cudaFreeAsync(prm.ws, s);
     return e;
 }
@@ -445,13 +465,15 @@ cudaError_t launch_ffma(const Problem &p, const Knobs &kn, cudaStream_t s) {
     // run 2-5% faster per flop than 128 x 128 (8 x 8: 4 per 32) at n = 8192
     // (profiles/r01_ab_ffma_bn256.txt) but halve the tile count, so take 256
     // unless 128 fills the persistent grid's waves better by more than that.
-    const int grid = kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms;
+    // (from the device's SM count, not opts.num_ctas: the split-K decision
+    // follows the tile count, and results must not depend on the grid)
+    const int grid = kn.num_sms;
     auto eff = [&](int bn, double kern) {
         const int64_t tiles = int64_t((p.M + BM - 1) / BM) * ((p.N + bn - 1) / bn);
         const int64_t waves = (tiles + grid - 1) / grid;
         return kern * double(tiles) / double(waves * grid) * double(p.N) / double(((p.N + bn - 1) / bn) * bn);
     };
-    if (eff(256, 1.04) >= eff(128, 1.0)) {
+    if (kn.tile_n == 256 || (kn.tile_n == 0 && eff(256, 1.04) >= eff(128, 1.0))) {
         if (AK && BKM)  return launch_t<true, true, 256>(p, kn, s);
         if (AK && !BKM) return launch_t<true, false, 256>(p, kn, s);
         if (!AK && BKM) return launch_t<false, true, 256>(p, kn, s);

@@ -64,7 +64,9 @@ lpy_status validate_all(int64_t M, int64_t N, int64_t K, const Operand &A, const
     if (opts) {
         if (opts->num_ctas < 0 || opts->raster_group < 0 || opts->promote_kblocks < 0)
             return LPY_ERR_INVALID_VALUE;
-        for (int i = 0; i < 5; ++i)
+        if (opts->tile_n != 0 && opts->tile_n != 128 && opts->tile_n != 192 && opts->tile_n != 256)
+            return LPY_ERR_INVALID_VALUE;
+        for (int i = 0; i < 4; ++i)
             if (opts->reserved[i] != 0) return LPY_ERR_INVALID_VALUE;
     }
     lpy_status s;
@@ -258,7 +260,12 @@ lpy_status lpy_gemm_f32_ex(int64_t M, int64_t N, int64_t K, const float *A, int6
 
     lpy::Problem prob{int(M), int(N), int(K), oa.p, oa.ld, oa.layout, ob.p, ob.ld, ob.layout, C, ldc};
     lpy::Knobs kn{opts ? opts->num_ctas : 0, opts ? opts->raster_group : 0, opts ? opts->promote_kblocks : 0,
-                  dev.sms};
+                  dev.sms, opts ? opts->tile_n : 0};
+    if (kn.tile_n == 192 && (chosen == LPY_PATH_FFMA || !lpy::tf32_supported(prob))) {
+        for (int i = 0; i < 2; ++i)
+            if (scratch[i]) cudaFreeAsync(scratch[i], s);
+        return LPY_ERR_NOT_SUPPORTED;
+    }
     if (chosen == LPY_PATH_3XTF32 && !lpy::tf32_supported(prob)) {
         st = (path == LPY_PATH_3XTF32) ? LPY_ERR_NOT_SUPPORTED : LPY_OK;
         if (st == LPY_OK) e = lpy::launch_ffma(prob, kn, s);

@@ -27,6 +27,7 @@ struct Knobs {
     int raster_group;     // 0 = auto
     int promote_kblocks;  // 0 = auto
     int num_sms;          // multiprocessor count of the current device
+    int tile_n;           // 0 = auto; else the output-tile width (validated by the front end)
 };
 
 // 2-D tensor map over a strided matrix: `inner` contiguous elements per line,

@@ -29,6 +29,18 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Release a stage the calling warp has been READING with LDS: ptxas issues
+// mbarrier.arrive without waiting on the scoreboards of shared loads still in
+// flight (measured: the FFMA consumer's last two LDS.128 of a k-block were
+// issued before its SYNCS.ARRIVE and consumed after it, so the producer could
+// refill the stage under them).  A CTA-scope fence first makes every memory
+// access of the warp complete; then one lane arrives.
+__device__ __forceinline__ void mbar_arrive_after_reads(uint64_t *bar, int lane) {
+    __syncwarp();
+    asm volatile("fence.acq_rel.cta;" ::: "memory");
+    if (lane == 0) mbar_arrive(bar);
+}
+
 // Block until the phase with parity `parity` of `bar` has completed.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(

@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_1405_7470_b200 as lpy  # noqa: E402
-from paper_1405_7470_b200.dist import chunk_bounds, chunk_grid, rowpanel_gemm  # noqa: E402
+from paper_1405_7470_b200.dist import chunk_bounds, chunk_grid, chunk_tile_n, rowpanel_gemm  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 G = int(sys.argv[2]) if len(sys.argv) > 2 else 8
@@ -51,6 +51,7 @@ for chunks in (2, 4, 8):
         def gemm_fn(a, b, c):
             o = lpy.GemmOpts()
             o.num_ctas = chunk_grid(a.shape[0], b.shape[1], sms, path)
+            o.tile_n = chunk_tile_n(path)
             lpy.gemm(a, b, out=c, path=path, opts=o)
 
         def step():

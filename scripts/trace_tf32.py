@@ -26,6 +26,10 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 promote = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 A = torch.randn(n, n, device="cuda")
 B = torch.randn(n, n, device="cuda")
+if os.environ.get("LA", "row") == "col":   # LA / LB = row|col: operand layouts
+    A = A.t().contiguous().t()
+if os.environ.get("LB", "row") == "col":
+    B = B.t().contiguous().t()
 opts = lpy.GemmOpts()
 opts.promote_kblocks = promote
 for _ in range(3):

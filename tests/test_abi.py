@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_version_and_status_strings():
-    assert lpy.lpy_version() == 3
+    assert lpy.lpy_version() == 4
     for code in range(10):
         s = lpy.lpy_status_string(code)
         assert s.startswith("LPY_")
@@ -81,6 +81,9 @@ def test_validation_errors_precede_cuda(kw, code):
 def test_bad_opts_rejected():
     o = lpy.GemmOpts()
     o.reserved[2] = 1
+    assert call(opts=o) == 1
+    o = lpy.GemmOpts()
+    o.tile_n = 100
     assert call(opts=o) == 1
     o = lpy.GemmOpts()
     o.num_ctas = -2

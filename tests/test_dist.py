@@ -49,7 +49,7 @@ def test_chunk_policy():
     # grids sized to a block's own tiles, never beyond the chip
     assert chunk_grid(1024, 1024, 148, "3xtf32") == 32      # 16 pair tiles
     assert chunk_grid(8192, 8192, 148, "3xtf32") == 148
-    assert chunk_grid(1024, 1024, 148, "ffma") == 64
+    assert chunk_grid(1024, 1024, 148, "ffma") == 32
     assert chunk_grid(1, 1, 148, "ffma") == 1
 
 
