@@ -246,7 +246,8 @@ def make_inputs(n, rank, world, chunks, device, owners=False, comm_world=None):
 def time_path(args, path, rank, world, device, dist_on):
     import torch
     import paper_1405_7470_b200 as lpy
-    from paper_1405_7470_b200.dist import choose_chunks, chunk_grid, chunk_streams, panel_bounds, rowpanel_gemm
+    from paper_1405_7470_b200.dist import (choose_chunks, chunk_grid, chunk_streams, chunk_tile_n, panel_bounds,
+                                          rowpanel_gemm)
     n = args.n
     pw = args.emulate_ranks if (args.emulate_ranks and world == 1) else world   # panel split
     r0_, r1_ = panel_bounds(n, pw, rank)
@@ -260,6 +261,7 @@ def time_path(args, path, rank, world, device, dist_on):
         if dist_on and len(bounds) > 1:
             opts = lpy.GemmOpts()
             opts.num_ctas = chunk_grid(a.shape[0], b.shape[1], sms, path)
+            opts.tile_n = chunk_tile_n(path)
         lpy.gemm(a, b, out=c, path=path, opts=opts)
 
     comm = torch.cuda.Stream() if dist_on else None

@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define LPY_VERSION 3
+#define LPY_VERSION 4
 
 typedef enum { LPY_ROW_MAJOR = 0, LPY_COL_MAJOR = 1 } lpy_layout;
 
@@ -93,7 +93,13 @@ typedef struct lpy_gemm_opts {
     int32_t raster_group;    /* output-tile rows per rasterisation group; 0 = auto   */
     int32_t promote_kblocks; /* 3xTF32: k-blocks per TMEM partial before promotion;  */
                              /* 0 = auto                                             */
-    int32_t reserved[5];     /* must be 0                                            */
+    int32_t tile_n;          /* output-tile width: 0 = auto (from shape and device), */
+                             /* else 128 or 256 (both paths) or 192 (3xTF32 only;    */
+                             /* LPY_ERR_NOT_SUPPORTED on FFMA); other values are     */
+                             /* LPY_ERR_INVALID_VALUE.  Results are identical for    */
+                             /* every tile width and grid size (each element's sum   */
+                             /* order is fixed by K alone)              */
+    int32_t reserved[4];     /* must be 0                                            */
 } lpy_gemm_opts;
 
 /* C := A * B on the device, enqueued on `stream` (see header comment).

@@ -46,7 +46,8 @@ def library_path() -> str:
 
 class GemmOpts(ctypes.Structure):
     _fields_ = [("num_ctas", ctypes.c_int32), ("raster_group", ctypes.c_int32),
-                ("promote_kblocks", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("promote_kblocks", ctypes.c_int32), ("tile_n", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 4)]
 
 
 class LpyError(RuntimeError):

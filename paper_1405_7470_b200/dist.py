@@ -68,13 +68,24 @@ def chunk_streams(rows: int, chunks: int) -> int:
     return max(1, min(want, chunks))
 
 
+def chunk_tile_n(path: str) -> int:
+    """Output-tile width (opts.tile_n) for a block product: full-width tiles
+    (256 x 256 per CTA pair on 3xTF32, 128 x 256 per CTA on FFMA) whatever
+    share of the GPU the block's grid gets; the automatic choice would look at
+    the block alone and pick narrower tiles to fill all SMs."""
+    del path
+    return 256
+
+
 def chunk_grid(rows: int, cols: int, sms: int, path: str) -> int:
     """Persistent grid (CTAs) for one block product sized to its own tiles
-    (256 x 256 per CTA pair on 3xTF32, 128 x 128 per CTA on FFMA), so
-    concurrent block products share the SMs instead of each claiming all."""
+    of width chunk_tile_n (256 x 256 per CTA pair on 3xTF32, 128 x 256 per CTA
+    on FFMA), so concurrent block products share the SMs instead of each
+    claiming all."""
+    tn = chunk_tile_n(path)
     if path == "3xtf32":
-        return 2 * max(1, min(sms // 2, math.ceil(rows / 256) * math.ceil(cols / 256)))
-    return max(1, min(sms, math.ceil(rows / 128) * math.ceil(cols / 128)))
+        return 2 * max(1, min(sms // 2, math.ceil(rows / 256) * math.ceil(cols / tn)))
+    return max(1, min(sms, math.ceil(rows / 128) * math.ceil(cols / tn)))
 
 
 def block_owner(c: int, world: int, root: int = 0, owners: bool = False) -> int:
