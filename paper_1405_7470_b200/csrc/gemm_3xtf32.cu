@@ -43,6 +43,7 @@
 namespace lpy {
 namespace tf32 {
 
+constexpr int MAX_SPLITS = 4;                // k-slices per split tile (tail_split caps S)
 constexpr int BM = 128, BK = 16;             // BM rows per CTA (the tile's BN columns: template, 128/192/256)
 constexpr int THREADS = 512;                 // 16 warps = 4 warpgroups
 constexpr int XFORM_WARP0 = 4, XFORM_WARPS = 4;
@@ -68,7 +69,8 @@ struct Params {
     float *C;
     int64_t ldc;
     int tiles_m, tiles_n, num_tiles, k_blocks, group, promote;
-    int c_vec;
+    int c_vec;          // C rows 16-byte aligned (float4 stores)
+    int c_vec8;         // C rows 32-byte aligned (STG.256)
     long long *trace;   // diagnostics build only (-DLPY_TRACE): per-CTA cycle counters
     // Tail split (the ragged last wave): tiles [0, full_tiles) are one work unit
     // each; every later tile is split into `splits` k-slices, so the last wave
@@ -100,9 +102,29 @@ __device__ __forceinline__ void unit_range(int u, const Params &p, int &t, int &
 #ifdef LPY_TRACE
 #define TR_T0(v) const long long v = clock64()
 #define TR_ADD(slot, v) (tr[slot] += clock64() - (v))
+// timeline of CTA 0: %globaltimer (ns) at event `slot`, after the counters
+#define TL(slot)                                                                      \
+    do {                                                                              \
+        if (p.trace && blockIdx.x == 0) {                                             \
+            unsigned long long g_;                                                    \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                    \
+            p.trace[gridDim.x * 8 + (slot)] = (long long)g_;                          \
+        }                                                                             \
+    } while (0)
+// every CTA's entry / exit time, after the timeline
+#define TLC(which)                                                                    \
+    do {                                                                              \
+        if (p.trace) {                                                                \
+            unsigned long long g_;                                                    \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                    \
+            p.trace[gridDim.x * 8 + 16 + 4 * blockIdx.x + (which)] = (long long)g_;   \
+        }                                                                             \
+    } while (0)
 #else
 #define TR_T0(v) (void)0
 #define TR_ADD(slot, v) (void)0
+#define TL(slot) (void)0
+#define TLC(which) (void)0
 #endif
 
 __device__ __forceinline__ void tile_coords(int t, const Params &p, int &tm, int &tn) {
@@ -133,6 +155,21 @@ __device__ __forceinline__ float tf32_small(float x) {
     const float big = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);   // what the MMA sees
     const uint32_t r = __float_as_uint(x - big);
     return __uint_as_float((r + 0x1000u) & 0xFFFFE000u);
+}
+
+// C[row, col .. col+7] = v (a row pointer `crow`), clipped at N: one STG.256
+// when C's rows are 32-byte aligned, else two float4 stores, else scalars.
+__device__ __forceinline__ void store_row8(const Params &p, float *crow, int col, const float *v) {
+    if (p.c_vec8 && col + 7 < p.N) {
+        st_v8(crow + col, v);
+    } else if (p.c_vec && col + 7 < p.N) {
+        *reinterpret_cast<float4 *>(crow + col) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4 *>(crow + col + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (col + e < p.N) crow[col + e] = v[e];
+    }
 }
 
 // Arrive (one per warp) on the leader CTA's copy of `bar`.
@@ -168,6 +205,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int unit0 = blockIdx.x / CG, units = gridDim.x / CG;   // this pair's first tile, stride
 
     if (threadIdx.x == 0) {
+        TL(0);
+        TLC(0);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&ready[s], CG * XFORM_WARPS);
@@ -187,6 +226,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) TL(1);
 #ifdef LPY_TRACE
     long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
@@ -228,6 +268,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         } else {
                             tma_load_2d(sb, &tmB, &full[s], k0, n0);
                         }
+                        if (kb == kb0 && u == unit0) TL(2);
                         if (++s == STAGES) { s = 0; ph ^= 1; }
                     }
                 }
@@ -264,6 +305,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     TR_T0(t_r);
                     mbar_wait(&ready[s], ph);
                     TR_ADD(1, t_r);
+                    if (kb == kb0 && u == unit0 && lane == 0) TL(4);
                     tc_fence_after();
                     const uint32_t d = tmem + b * 256;
                     const uint64_t off = uint64_t(s) * STEP;
@@ -280,6 +322,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         }
                         umma_commit_cg<CG>(&empty[s]);
                         if (last) umma_commit_cg<CG>(&accf[b]);
+                        TL(5);
                     }
                     __syncwarp();
                     if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -302,6 +345,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 TR_T0(t_f);
                 mbar_wait(&full[s], ph);
                 TR_ADD(4, t_f);
+                if (kb == kb0 && u == unit0 && xt == 0) TL(3);
                 TR_T0(t_x);
                 const float4 *src = reinterpret_cast<const float4 *>(stages + s * STAGE_BYTES);
                 float4 *dst = reinterpret_cast<float4 *>(stages + s * STAGE_BYTES + RAW_BYTES);
@@ -342,6 +386,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 TR_T0(t_w);
                 mbar_wait(&accf[b], (np >> 1) & 1);
                 TR_ADD(5, t_w);
+                if (np == 0 && ept == 0) TL(6);
                 TR_T0(t_b);
                 tc_fence_after();
                 const uint32_t base = tmem + lane_base + b * 256 + half * EC;
@@ -362,53 +407,69 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (lane == 0) arrive_leader<CG>(&acce[b]);
                 TR_ADD(7, t_b);
             }
+            // one row per thread (TMEM lane = row), written with 32-byte stores so
+            // each instruction writes whole sectors of 32 rows
+            // (computed where used: live across the partial's write they cost
+            // the BN = 256 variants register spills)
+            if (ept == 0) TL(9);
+            auto row_of = [&]() {
+                int tm, tn;
+                tile_coords(t, p, tm, tn);
+                return tm * (BM * CG) + rank * BM + quad * 32 + lane;
+            };
+            auto col0_of = [&]() {
+                int tm, tn;
+                tile_coords(t, p, tm, tn);
+                return tn * BN + half * EC;
+            };
             if (su >= 0) {
-                // split tile: park this slice's partial (thread-interleaved float4s,
-                // a warp writes 512 contiguous bytes), count arrivals per (tile,
-                // CTA); the last slice sums all partials in slice order and stores.
-                constexpr int TILE4 = BM * BN / 4;
-                float4 *mine = reinterpret_cast<float4 *>(p.ws) + (int64_t(su) * CG + rank) * TILE4 + ept;
+                // split tile: park this slice's partial as thread-interleaved
+                // 32-byte vectors (a warp writes 1 KB contiguous), count arrivals
+                // per (tile, CTA); the last slice sums all partials in slice order
+                // and stores.
+                constexpr int TILE8 = BM * BN / 8;
+                float *mine = p.ws + ((int64_t(su) * CG + rank) * TILE8 + ept) * 8;
 #pragma unroll
-                for (int j = 0; j < EC; j += 4)
-                    __stcg(mine + (j / 4) * 256, make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
+                for (int j = 0; j < EC; j += 8) st_cg_v8(mine + (j / 8) * 256 * 8, &acc[j]);
+                if (ept == 0) TL(10);
                 __threadfence();
                 named_bar_sync(1, EPI_WARPS * 32);
+                if (ept == 0) TL(11);
                 const int vt = t - p.full_tiles;
                 if (ept == 0) last_flag = (atomicAdd(p.sem + vt * CG + rank, 1) == p.splits - 1);
                 named_bar_sync(1, EPI_WARPS * 32);
                 if (!last_flag) continue;
+                if (ept == 0) TLC(2);
                 __threadfence();
-                const float4 *base = reinterpret_cast<const float4 *>(p.ws) +
-                                     (int64_t(vt) * p.splits * CG + rank) * TILE4 + ept;
+                // sum the slices in slice order into acc (the own partial is
+                // re-read like the others), slice by slice so that all of a
+                // slice's loads are in flight at once: one SM pulls only ~50 GB/s
+                // from L2 (bytes in flight / latency), so the fix-up costs
+                // ~2.5 us per 128 KB partial
+                const float4 *base = reinterpret_cast<const float4 *>(
+                    p.ws + ((int64_t(vt) * p.splits * CG + rank) * TILE8 + ept) * 8);
+                const int64_t slice4 = int64_t(CG) * TILE8 * 2;
 #pragma unroll
                 for (int j = 0; j < EC; j += 4) {
-                    float4 a4 = __ldcg(base + (j / 4) * 256);
-                    for (int sl = 1; sl < p.splits; ++sl) {
-                        const float4 q = __ldcg(base + int64_t(sl) * CG * TILE4 + (j / 4) * 256);
-                        a4.x += q.x; a4.y += q.y; a4.z += q.z; a4.w += q.w;
-                    }
-                    acc[j] = a4.x; acc[j + 1] = a4.y; acc[j + 2] = a4.z; acc[j + 3] = a4.w;
+                    const float4 q = __ldcg(base + (j / 8) * 256 * 2 + (j % 8) / 4);
+                    acc[j] = q.x; acc[j + 1] = q.y; acc[j + 2] = q.z; acc[j + 3] = q.w;
                 }
+#pragma unroll 1
+                for (int sl = 1; sl < p.splits; ++sl) {
+#pragma unroll
+                    for (int j = 0; j < EC; j += 4) {
+                        const float4 q = __ldcg(base + sl * slice4 + (j / 8) * 256 * 2 + (j % 8) / 4);
+                        acc[j] += q.x; acc[j + 1] += q.y; acc[j + 2] += q.z; acc[j + 3] += q.w;
+                    }
+                }
+                if (ept == 0) { TL(12); TLC(3); }
                 if (ept == 0) p.sem[vt * CG + rank] = 0;   // ready for the next launch
             }
-            int tm, tn;
-            tile_coords(t, p, tm, tn);
-            const int row = tm * (BM * CG) + rank * BM + quad * 32 + lane;
+            const int row = row_of(), col0 = col0_of();
+            float *crow = p.C + int64_t(row) * p.ldc;
             if (row < p.M) {
-                float *crow = p.C + int64_t(row) * p.ldc;
-                const int col0 = tn * BN + half * EC;
 #pragma unroll
-                for (int j = 0; j < EC; j += 4) {
-                    const int col = col0 + j;
-                    if (p.c_vec && col + 3 < p.N) {
-                        *reinterpret_cast<float4 *>(crow + col) =
-                            make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            if (col + e < p.N) crow[col + e] = acc[j + e];
-                    }
-                }
+                for (int j = 0; j < EC; j += 8) store_row8(p, crow, col0 + j, &acc[j]);
             }
         }
     }
@@ -419,9 +480,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                                  (unsigned long long)tr[i]);
 #endif
 
+    if (threadIdx.x == EPI_WARP0 * 32) TL(7);
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     if (warp == 1) tmem_dealloc_cg<CG>(tmem, TMEM_COLS);
+    if (threadIdx.x == 32) { TL(8); TLC(1); }
 }
 
 template <int CG, bool AMN, bool BMN, int BN>
@@ -454,26 +517,65 @@ static cudaError_t launch_t(const CUtensorMap &ta, const CUtensorMap &tb, const 
 
 static long long *g_trace = nullptr;   // set by lpy_trace_set_buffer (diagnostics build)
 
+// Split of the last wave into k-slices, fixed by the shape and the device
+// (never by opts.num_ctas, so results stay bitwise grid-invariant):
+//  * >= 2 waves with a partial last one: its `rem` tiles are cut into
+//    S = floor(pairs / rem) slices (<= 4, >= 16 k-blocks each), so the last
+//    wave is S times shorter;
+//  * a single under-filled wave (tiles < pairs, e.g. n = 1024) is NOT split by
+//    default: cutting every tile into S = floor(pairs / tiles) slices fills the
+//    CTA pairs, but the last arriver's fix-up (S partials of 128 KB read by one
+//    SM at ~50 GB/s, then the tile stored) costs more than the k-loop saves --
+//    measured at n = 1024: 28.2 us unsplit (BN = 128) vs 32.9-38.8 us split
+//    S = 4 (BN = 256) in graph replay (profiles/r01_tf32_split1.txt).
+//    LPY_TF32_SPLIT1=1 enables it (diagnostics / A-B).
+struct TailSplit { int splits, full_tiles, num_units; };
+static TailSplit tail_split(int num_tiles, int k_blocks, int pairs) {
+    static const bool split1 = [] {
+        const char *e = getenv("LPY_TF32_SPLIT1");
+        return e && e[0] == '1';
+    }();
+    TailSplit r{1, num_tiles, num_tiles};
+    if (num_tiles <= 0 || pairs <= 0) return r;
+    const int waves = (num_tiles + pairs - 1) / pairs;
+    const int rem = num_tiles - (waves - 1) * pairs;
+    int S = pairs / rem;
+    if (S > MAX_SPLITS) S = MAX_SPLITS;
+    const int min_kb = waves >= 2 ? 16 : 8;
+    while (S > 1 && k_blocks / S < min_kb) --S;
+    if (S < 2 || (waves < 2 && !split1)) return r;
+    r.splits = S;
+    r.full_tiles = (waves - 1) * pairs;
+    r.num_units = r.full_tiles + (num_tiles - r.full_tiles) * S;
+    return r;
+}
+
 // Tile width for a CTA-pair product (256-row tiles): the BN in {256, 192, 128}
-// maximising (wave efficiency of its tiles on `pairs` persistent CTA pairs) x
-// (columns not wasted by a ragged last tile) x (the kernel's measured per-flop
-// efficiency at that width relative to 256: 0.86 for 192, 0.69 for 128 at
-// n = 8192 -- narrower MMAs leave the fixed per-k-block work (the A tile's TMA
-// and split) less time to hide in; profiles/r01_tf32_bn_sweep.txt).
-// n >= 4096 -> 256; n = 1024 -> 128 (32 tiles instead of 16); the ragged
-// config -> 192 (64 tiles instead of 48).
-int choose_bn(int M, int N, int pairs) {
+// minimising the modelled time of the schedule it gives on `pairs` persistent
+// CTA pairs: (unit waves) x (k-blocks per unit) x BN / (the kernel's measured
+// per-flop efficiency at that width relative to 256: 0.86 for 192, 0.69 for
+// 128 at n = 8192 -- narrower MMAs leave the fixed per-k-block work (the A
+// tile's TMA and split) less time to hide in; profiles/r01_tf32_bn_sweep.txt),
+// over the useful columns; narrower wins only by > 3%.  n >= 4096 -> 256;
+// n = 1024 -> 128 (32 tiles instead of 16); the ragged config -> 192 (64 tiles
+// instead of 48).
+int choose_bn(int M, int N, int K, int pairs) {
     const int64_t tm = (M + 2 * BM - 1) / (2 * BM);
-    auto eff = [&](int bn) {
+    const int kb = (K + BK - 1) / BK;
+    auto cost = [&](int bn) {
         const int64_t tn = (N + bn - 1) / bn, tiles = tm * tn;
-        const int64_t waves = (tiles + pairs - 1) / pairs;
+        const TailSplit ts = tail_split(int(tiles), kb, pairs);
         const double kern = bn == 256 ? 1.0 : bn == 192 ? 0.86 : 0.69;
-        return kern * double(tiles) / double(waves * pairs) * double(N) / double(tn * bn);
+        // whole-tile waves, then the split units' waves at 1/S of a tile each
+        const int64_t full_waves = (ts.full_tiles + pairs - 1) / pairs;
+        const int64_t split_units = ts.num_units - ts.full_tiles;
+        const double split_waves = double((split_units + pairs - 1) / pairs) / ts.splits;
+        return (double(full_waves) + split_waves) * bn / kern * double(tn * bn) / double(N);
     };
     int best = 256;
-    double best_eff = eff(256);
+    double best_cost = cost(256);
     for (int bn : {192, 128})
-        if (eff(bn) > best_eff * 1.03) { best = bn; best_eff = eff(bn); }
+        if (cost(bn) * 1.03 < best_cost) { best = bn; best_cost = cost(bn); }
     return best;
 }
 
@@ -501,22 +603,13 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, cudaStream_t s) 
     prm.group = kn.raster_group > 0 ? kn.raster_group : 16 / CG;
     prm.promote = kn.promote_kblocks > 0 ? kn.promote_kblocks : 8;   // 128 of K per TMEM partial
     prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
+    prm.c_vec8 = ((reinterpret_cast<uintptr_t>(p.C) & 31) == 0) && (p.ldc % 8 == 0);
     prm.trace = g_trace;
-    // Tail split, fixed by the shape and the device (never by opts.num_ctas, so
-    // results stay bitwise grid-invariant): when the last of >= 2 waves is
-    // partial, its `rem` tiles are cut into S = floor(pairs / rem) k-slices
-    // (<= 4, >= 16 k-blocks each) so the last wave is S times shorter.
     {
-        const int pairs = kn.num_sms / CG;
-        const int waves = (prm.num_tiles + pairs - 1) / pairs;
-        const int rem = prm.num_tiles - (waves - 1) * pairs;
-        int S = rem > 0 ? pairs / rem : 1;
-        if (S > 4) S = 4;
-        while (S > 1 && prm.k_blocks / S < 16) --S;
-        if (waves < 2 || S < 2) S = 1;
-        prm.splits = S;
-        prm.full_tiles = S > 1 ? (waves - 1) * pairs : prm.num_tiles;
-        prm.num_units = prm.full_tiles + (prm.num_tiles - prm.full_tiles) * S;
+        const TailSplit ts = tail_split(prm.num_tiles, prm.k_blocks, kn.num_sms / CG);
+        prm.splits = ts.splits;
+        prm.full_tiles = ts.full_tiles;
+        prm.num_units = ts.num_units;
     }
     prm.ws = nullptr;
     prm.sem = nullptr;
@@ -566,7 +659,7 @@ cudaError_t launch_3xtf32(const Problem &p, const Knobs &kn, cudaStream_t s) {
     // or from opts.tile_n (dist.py's per-chunk products, which share the GPU,
     // ask for full-width tiles)
     const int pairs = kn.num_sms / 2;
-    const int bn = kn.tile_n ? kn.tile_n : force_bn ? force_bn : tf32::choose_bn(p.M, p.N, pairs > 0 ? pairs : 1);
+    const int bn = kn.tile_n ? kn.tile_n : force_bn ? force_bn : tf32::choose_bn(p.M, p.N, p.K, pairs > 0 ? pairs : 1);
     switch (bn) {
         case 128: return tf32::launch_cg<2, 128>(p, kn, s);
         case 192: return tf32::launch_cg<2, 192>(p, kn, s);

@@ -35,7 +35,7 @@ opts.promote_kblocks = promote
 for _ in range(3):
     lpy.gemm(A, B, path="3xtf32", opts=opts)
 sms = torch.cuda.get_device_properties(0).multi_processor_count
-buf = torch.zeros(sms * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(sms * 8 + 16 + 4 * sms, dtype=torch.int64, device="cuda")
 lib.lpy_trace_set_buffer(buf.data_ptr())
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
@@ -43,7 +43,30 @@ lpy.gemm(A, B, path="3xtf32", opts=opts)
 e1.record()
 torch.cuda.synchronize()
 lib.lpy_trace_set_buffer(None)
-t = buf.view(sms, 8).double()
+grid = int(os.environ.get("GRID", "0")) or sms   # CTAs launched (timeline slots follow grid*8 counters)
+tl = buf[grid * 8: grid * 8 + 13].cpu().tolist()
+ev = ["entry", "setup synced", "first TMA issued", "first stage transformed-in (xform saw full)", "MMA saw first ready",
+      "MMA last commit issued", "epilogue saw first accf", "epilogue done", "exit (after cluster sync+dealloc)",
+      "epilogue: last TMEM partial read", "split: partial written", "split: fenced + barrier", "split: fix-up sum read"]
+if tl[0]:
+    print("CTA 0 timeline (us from entry):")
+    for name, v in zip(ev, tl):
+        print(f"  {name:44s} {(v - tl[0]) / 1e3 if v else float('nan'):8.2f}")
+ce4 = buf[grid * 8 + 16: grid * 8 + 16 + 4 * grid].view(grid, 4).double()
+ce = ce4[:, :2]
+if ce[0, 0] > 0:
+    t0 = ce[:, 0].min()
+    st, en = (ce[:, 0] - t0) / 1e3, (ce[:, 1] - t0) / 1e3
+    print(f"per-CTA (us from first entry): entry min/med/max {st.min():.2f}/{st.median():.2f}/{st.max():.2f}, "
+          f"exit min/med/max {en.min():.2f}/{en.median():.2f}/{en.max():.2f}")
+    order = torch.argsort(en)
+    print("  slowest CTAs (id: entry-exit):", ", ".join(f"{int(i)}: {st[i]:.1f}-{en[i]:.1f}" for i in order[-6:]))
+    fx = ce4[:, 2] > 0
+    if fx.any():
+        f0, f1 = (ce4[fx, 2] - t0) / 1e3, (ce4[fx, 3] - t0) / 1e3
+        print(f"  fix-up CTAs: {int(fx.sum())}, start min/med/max {f0.min():.2f}/{f0.median():.2f}/{f0.max():.2f}, "
+              f"loads done min/med/max {f1.min():.2f}/{f1.median():.2f}/{f1.max():.2f}, exit max {en[fx].max():.2f}")
+t = buf[: sms * 8].view(sms, 8).double()
 lead = t[t[:, 0] > 0]
 names = ["mma_total", "mma_wait_ready", "mma_wait_acce", "prod_wait_empty", "xform_wait_full",
          "epi_wait_accf", "xform_busy", "epi_busy"]
