@@ -168,20 +168,36 @@ def operand_layout(x):
     return None
 
 
-def _stream_handle(stream):
+def _stream_handle(stream, device_index=None):
+    """cudaStream_t of `stream` (a torch.cuda.Stream or a raw handle), or of
+    the current stream of `device_index` (default: the current device)."""
     import torch
     if stream is None:
-        stream = torch.cuda.current_stream()
+        if device_index is None:
+            device_index = torch.cuda.current_device()
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)   # no Stream object: ~1 us cheaper
+        return raw(device_index) if raw is not None else torch.cuda.current_stream(device_index).cuda_stream
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
 def _one_device(*tensors):
     """The single CUDA device all `tensors` live on (the C ABI works on the
     current device, so calls run under a guard for it); raises otherwise."""
-    devs = {t.device for t in tensors}
-    if len(devs) != 1 or next(iter(devs)).type != "cuda":
-        raise ValueError(f"all operands must be on one CUDA device, got {sorted(map(str, devs))}")
-    return next(iter(devs))
+    dev = tensors[0].device
+    if dev.type != "cuda" or any(t.device != dev for t in tensors[1:]):
+        raise ValueError(f"all operands must be on one CUDA device, got {sorted({str(t.device) for t in tensors})}")
+    return dev
+
+
+def _on_device(tensors, stream, call):
+    """call(stream handle) with the tensors' device current: the guard is only
+    entered when that device is not already current (it costs microseconds)."""
+    import torch
+    idx = _one_device(*tensors).index
+    if idx is None or idx == torch.cuda.current_device():
+        return call(_stream_handle(stream, idx))
+    with torch.cuda.device(idx):
+        return call(_stream_handle(stream, idx))
 
 
 def _path_id(path) -> int:
@@ -215,9 +231,11 @@ def gemm(A, B, out=None, path="auto", stream=None, opts: GemmOpts | None = None)
     lc = operand_layout(out)
     if lc is None:
         raise ValueError("out must be row- or column-major")
-    with torch.cuda.device(_one_device(A, B, out)):
-        st = lpy_gemm_f32_ex(M, N, K, A.data_ptr(), la[1], la[0], B.data_ptr(), lb[1], lb[0],
-                             out.data_ptr(), lc[1], lc[0], _stream_handle(stream), _path_id(path), opts)
+    lib = _lib or load_library()
+    po = ctypes.byref(opts) if opts is not None else None
+    st = _on_device((A, B, out), stream, lambda sh: lib.lpy_gemm_f32_ex(
+        M, N, K, A.data_ptr(), la[1], la[0], B.data_ptr(), lb[1], lb[0], out.data_ptr(), lc[1], lc[0], sh,
+        _path_id(path), po))
     if st != 0:
         raise LpyError(st, "lpy_gemm_f32_ex")
     return out
@@ -256,9 +274,8 @@ def saxpy(alpha, x, y, stream=None):
         raise ValueError("device tensors required (use saxpy_host for host buffers)")
     import torch
     incx, incy = _vec(x, "x"), _vec(y, "y")
-    with torch.cuda.device(_one_device(x, y)):
-        st = lpy_saxpy_f32(x.shape[0], float(alpha), x.data_ptr(), incx, y.data_ptr(), incy,
-                           _stream_handle(stream))
+    st = _on_device((x, y), stream, lambda sh: lpy_saxpy_f32(x.shape[0], float(alpha), x.data_ptr(), incx,
+                                                             y.data_ptr(), incy, sh))
     if st != 0:
         raise LpyError(st, "lpy_saxpy_f32")
     return y
@@ -297,9 +314,9 @@ def coulomb(targets, sources, charges, out=None, stream=None):
     nt = targets.shape[0]
     if out is None:
         out = torch.empty(nt, dtype=torch.float32, device=targets.device)
-    with torch.cuda.device(_one_device(targets, sources, charges, out)):
-        st = lpy_coulomb_f32(nt, targets.data_ptr(), ldt, sources.shape[0], sources.data_ptr(), lds,
-                             charges.data_ptr(), out.data_ptr(), _stream_handle(stream))
+    st = _on_device((targets, sources, charges, out), stream, lambda sh: lpy_coulomb_f32(
+        nt, targets.data_ptr(), ldt, sources.shape[0], sources.data_ptr(), lds, charges.data_ptr(),
+        out.data_ptr(), sh))
     if st != 0:
         raise LpyError(st, "lpy_coulomb_f32")
     return out

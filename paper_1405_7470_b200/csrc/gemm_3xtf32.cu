@@ -493,13 +493,8 @@ static cudaError_t launch_t(const CUtensorMap &ta, const CUtensorMap &tb, const 
     using C_ = Cfg<CG, BN>;
     static_assert(C_::EC % 32 == 0 && C_::SMEM_BYTES <= 227 * 1024, "tile does not fit");
     auto kern = gemm_3xtf32_kernel<CG, AMN, BMN, BN>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(C_::SMEM_BYTES));
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
+    static std::atomic<uint64_t> attr_done{0};
+    if (cudaError_t e = ensure_smem_attr(kern, int(C_::SMEM_BYTES), attr_done); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(THREADS);

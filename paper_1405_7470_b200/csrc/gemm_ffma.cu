@@ -422,11 +422,11 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     }
 
     auto kern = prm.splits > 1 ? gemm_ffma_kernel<AK, BKM, BN, true> : gemm_ffma_kernel<AK, BKM, BN, false>;
-    static bool attr_done[2] = {false, false};  // benign race: setting the attribute twice is harmless
-    if (!attr_done[prm.splits > 1]) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::SMEM_BYTES));
-        if (e != cudaSuccess) return e;
-        attr_done[prm.splits > 1] = true;
+    static std::atomic<uint64_t> attr_done[2];
+    e = ensure_smem_attr(kern, int(G::SMEM_BYTES), attr_done[prm.splits > 1]);
+    if (e != cudaSuccess) {
+        if (prm.ws) cudaFreeAsync(prm.ws, s);
+        return e;
     }
     kern<<<grid, G::THREADS, G::SMEM_BYTES, s>>>(ta, tb, prm);
     e = cudaGetLastError();

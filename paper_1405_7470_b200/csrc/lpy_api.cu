@@ -156,8 +156,50 @@ static PFN_encodeTiled get_encode() {
     return fn;
 }
 
+// Encoded descriptors are cached (a call re-using the buffers of an earlier one
+// -- a training or benchmark loop -- skips cuTensorMapEncodeTiled, which costs
+// about as much host time as the launch).  A descriptor holds only the address
+// and geometry, so an entry stays valid whatever happens to the memory behind
+// it; the cache is a small direct-mapped table under a mutex.
+namespace {
+struct TmapKey {
+    const float *base;
+    uint64_t inner, outer, ld;
+    uint32_t box_inner, box_outer;
+    int swizzle;
+    bool operator==(const TmapKey &o) const {
+        return base == o.base && inner == o.inner && outer == o.outer && ld == o.ld && box_inner == o.box_inner &&
+               box_outer == o.box_outer && swizzle == o.swizzle;
+    }
+};
+struct TmapEntry {
+    bool used = false;
+    TmapKey key{};
+    CUtensorMap map{};
+};
+constexpr int kTmapCache = 64;
+std::mutex tmap_mu;
+TmapEntry tmap_cache[kTmapCache];
+
+size_t tmap_slot(const TmapKey &k) {
+    uint64_t h = reinterpret_cast<uintptr_t>(k.base) >> 8;
+    for (uint64_t v : {k.inner, k.outer, k.ld, uint64_t(k.box_inner) << 32 | k.box_outer, uint64_t(k.swizzle)})
+        h = (h ^ v) * 0x9E3779B97F4A7C15ull;
+    return size_t(h >> 58) % kTmapCache;
+}
+}  // namespace
+
 cudaError_t make_tmap_2d(CUtensorMap *tm, const float *base, uint64_t inner, uint64_t outer, uint64_t ld,
                          uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swizzle) {
+    const TmapKey key{base, inner, outer, ld, box_inner, box_outer, int(swizzle)};
+    const size_t slot = tmap_slot(key);
+    {
+        std::lock_guard<std::mutex> g(tmap_mu);
+        if (tmap_cache[slot].used && tmap_cache[slot].key == key) {
+            *tm = tmap_cache[slot].map;
+            return cudaSuccess;
+        }
+    }
     PFN_encodeTiled enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
     cuuint64_t dims[2] = {inner, outer};
@@ -168,7 +210,12 @@ cudaError_t make_tmap_2d(CUtensorMap *tm, const float *base, uint64_t inner, uin
                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      swizzle,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> g(tmap_mu);
+    tmap_cache[slot].used = true;
+    tmap_cache[slot].key = key;
+    tmap_cache[slot].map = *tm;
+    return cudaSuccess;
 }
 
 }  // namespace lpy

@@ -1,5 +1,6 @@
 // Internal interface between the C-ABI front end (lpy_api.cu) and the kernels.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -21,6 +22,22 @@ struct Problem {
     float *C;
     int64_t ldc;
 };
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `kern` on the current
+// device, once per device (function attributes are per device context; a
+// process-wide "done" flag would skip the second GPU of a multi-GPU process).
+// `done` is a per-kernel bitmask of devices already configured.
+template <class F>
+inline cudaError_t ensure_smem_attr(F kern, int bytes, std::atomic<uint64_t> &done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
 
 struct Knobs {
     int num_ctas;         // 0 = auto
