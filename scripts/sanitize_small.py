@@ -28,6 +28,12 @@ for path in ("ffma", "3xtf32"):
                              ldb=synth.min_ld(K, N, lb), ldc=synth.min_ld(M, N, lc) + 1, path=path)
         assert pad_ok
         worst = max(worst, check(C, A, B))
+    # C rows 16-byte but not 32-byte aligned (ldc % 8 == 4): the float4 store path
+    A = synth.matrix(300, 130, seed=3, matrix_id=0)
+    B = synth.matrix(130, 200, seed=3, matrix_id=1)
+    C, pad_ok = run_gemm(A, B, 0, 0, 0, ldc=204, path=path)
+    assert pad_ok
+    worst = max(worst, check(C, A, B))
 print(f"sanitize_small: all products within tolerance (worst {worst:.2e})")
 
 # split-K FFMA (under-filled grid: 72 tiles -> 2 slices) and the 3xTF32 tail
