@@ -339,14 +339,21 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
     }
 }
 
-// Split-K fix-up: one CTA of 256 threads per output tile; thread ctid owns the
-// elements consumer thread ctid of the GEMM kernel owned (same a_row / b_col
-// map), adds the tile's slice partials in slice order and stores C with the
-// same ragged-edge predicates.
+// Split-K fix-up: FIXUP_PARTS CTAs of 256 threads per output tile, part r
+// taking micro-tile rows i in [r * 8 / FIXUP_PARTS, (r + 1) * 8 / FIXUP_PARTS);
+// thread ctid owns the elements consumer thread ctid of the GEMM kernel owned
+// (same a_row / b_col map), adds the tile's slice partials in slice order and
+// stores C with the same ragged-edge predicates.  Several CTAs per tile: one
+// SM pulls only ~50 GB/s of partials from L2 (bytes in flight / latency), so
+// the fix-up is spread over more SMs than there are tiles.
+constexpr int FIXUP_PARTS = 4;
+constexpr int MAX_SPLITS = 8;     // choose_splits' cap for this path
 template <int BN>
 __global__ void __launch_bounds__(CWARPS * 32) splitk_fixup_kernel(const Params p) {
     constexpr int JN = BN / 32, PER = 8 * JN / 2;
+    constexpr int IPART = 8 / FIXUP_PARTS;
     const int t = blockIdx.x;
+    const int i0 = blockIdx.y * IPART;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wm = warp >> 2, wn = warp & 3, lm = lane >> 2, ln = lane & 3;
     int tm, tn;
@@ -355,15 +362,19 @@ __global__ void __launch_bounds__(CWARPS * 32) splitk_fixup_kernel(const Params 
                          threadIdx.x * PER;
     const int m0 = tm * BM, n0 = tn * BN;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int ii = 0; ii < IPART; ++ii) {
+        const int i = i0 + ii;
         const int row = m0 + a_row(wm, lm, i);
         float acc[2 * JN];
 #pragma unroll
         for (int h = 0; h < JN / 2; ++h) {
             float4 s0 = base[i * (JN / 2) + h];
-            for (int sl = 1; sl < p.splits; ++sl) {
-                const float4 q = base[int64_t(sl) * (BM * BN / 4) + i * (JN / 2) + h];
-                s0.x += q.x; s0.y += q.y; s0.z += q.z; s0.w += q.w;
+#pragma unroll
+            for (int sl = 1; sl < MAX_SPLITS; ++sl) {   // unrolled: every slice's load in flight
+                if (sl < p.splits) {
+                    const float4 q = base[int64_t(sl) * (BM * BN / 4) + i * (JN / 2) + h];
+                    s0.x += q.x; s0.y += q.y; s0.z += q.z; s0.w += q.w;
+                }
             }
             acc[4 * h] = s0.x; acc[4 * h + 1] = s0.y; acc[4 * h + 2] = s0.z; acc[4 * h + 3] = s0.w;
         }
@@ -406,7 +417,7 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     prm.k_blocks = (p.K + BK - 1) / BK;
     prm.group = kn.raster_group > 0 ? kn.raster_group : 16;
     prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
-    prm.splits = choose_splits(prm.num_tiles, prm.k_blocks, kn.num_sms, 4, 8);
+    prm.splits = choose_splits(prm.num_tiles, prm.k_blocks, kn.num_sms, 4, MAX_SPLITS);
     prm.num_units = prm.num_tiles * prm.splits;
     prm.ws = nullptr;
     int grid = kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms;
@@ -431,7 +442,7 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     kern<<<grid, G::THREADS, G::SMEM_BYTES, s>>>(ta, tb, prm);
     e = cudaGetLastError();
     if (e == cudaSuccess && prm.splits > 1) {
-        splitk_fixup_kernel<BN><<<prm.num_tiles, CWARPS * 32, 0, s>>>(prm);
+        splitk_fixup_kernel<BN><<<dim3(prm.num_tiles, FIXUP_PARTS), CWARPS * 32, 0, s>>>(prm);
         e = cudaGetLastError();
     }
     if (prm.ws) cudaFreeAsync(prm.ws, s);
