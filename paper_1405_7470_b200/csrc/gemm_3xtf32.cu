@@ -70,6 +70,7 @@ struct Params {
     int64_t ldc;
     int tiles_m, tiles_n, num_tiles, k_blocks, group, promote;
     int c_vec;          // C rows 16-byte aligned (float4 stores)
+    int l2hint;         // 0: no L2 hints; 1: A evict_last, B evict_first; 2: the reverse
     int c_vec8;         // C rows 32-byte aligned (STG.256)
     long long *trace;   // diagnostics build only (-DLPY_TRACE): per-CTA cycle counters
     // Tail split (the ragged last wave): tiles [0, full_tiles) are one work unit
@@ -238,6 +239,12 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (lane == 0) {
                 tma_prefetch_desc(&tmA);
                 tma_prefetch_desc(&tmB);
+                const uint64_t pol_a = p.l2hint == 1 ? l2_policy_evict_last() : l2_policy_evict_first();
+                const uint64_t pol_b = p.l2hint == 1 ? l2_policy_evict_first() : l2_policy_evict_last();
+                auto load = [&](void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1, uint64_t pol) {
+                    if (p.l2hint) tma_load_2d_hint(dst, tm, bar, c0, c1, pol);
+                    else          tma_load_2d(dst, tm, bar, c0, c1);
+                };
                 int s = 0;
                 uint32_t ph = 0;
                 for (int u = unit0; u < p.num_units; u += units) {
@@ -257,16 +264,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                         if constexpr (AMN) {
 #pragma unroll
                             for (int j = 0; j < BM / 32; ++j)
-                                tma_load_2d(sa + j * 2048, &tmA, &full[s], m0 + 32 * j, k0);
+                                load(sa + j * 2048, &tmA, &full[s], m0 + 32 * j, k0, pol_a);
                         } else {
-                            tma_load_2d(sa, &tmA, &full[s], k0, m0);
+                            load(sa, &tmA, &full[s], k0, m0, pol_a);
                         }
                         if constexpr (BMN) {
 #pragma unroll
                             for (int j = 0; j < C_::BN_CTA / 32; ++j)
-                                tma_load_2d(sb + j * 2048, &tmB, &full[s], n0 + 32 * j, k0);
+                                load(sb + j * 2048, &tmB, &full[s], n0 + 32 * j, k0, pol_b);
                         } else {
-                            tma_load_2d(sb, &tmB, &full[s], k0, n0);
+                            load(sb, &tmB, &full[s], k0, n0, pol_b);
                         }
                         if (kb == kb0 && u == unit0) TL(2);
                         if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -599,6 +606,11 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, cudaStream_t s) 
     prm.promote = kn.promote_kblocks > 0 ? kn.promote_kblocks : 8;   // 128 of K per TMEM partial
     prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
     prm.c_vec8 = ((reinterpret_cast<uintptr_t>(p.C) & 31) == 0) && (p.ldc % 8 == 0);
+    static const int l2hint = [] {   // LPY_L2HINT=0|1|2 (diagnostics / A-B)
+        const char *e = getenv("LPY_L2HINT");
+        return e ? atoi(e) : 0;
+    }();
+    prm.l2hint = l2hint;
     prm.trace = g_trace;
     {
         const TailSplit ts = tail_split(prm.num_tiles, prm.k_blocks, kn.num_sms / CG);

@@ -150,6 +150,17 @@ __device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap *tm, int32_
                  "r"(c0), "r"(c1)
                  : "memory");
 }
+// L2 eviction-priority policies for the .L2::cache_hint loads below.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 // Same with an L2 cache-policy hint (createpolicy result).
 __device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *tm, uint64_t *bar,
                                                  int32_t c0, int32_t c1, uint64_t policy) {
