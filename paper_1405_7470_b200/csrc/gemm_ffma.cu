@@ -34,6 +34,7 @@
 // Accumulation is fp32 FFMA (RN) with k ascending per element, identical for
 // every layout.
 #include <cstdio>
+#include <cstdlib>
 #include "lpy_internal.h"
 #include "ptx.cuh"
 
@@ -417,7 +418,15 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     prm.k_blocks = (p.K + BK - 1) / BK;
     prm.group = kn.raster_group > 0 ? kn.raster_group : 16;
     prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
-    prm.splits = choose_splits(prm.num_tiles, prm.k_blocks, kn.num_sms, 4, MAX_SPLITS);
+    // k-blocks per slice at least: 1 -- a 128^3 product (one tile, 4 k-blocks)
+    // then runs as 4 slices on 4 SMs: 13.8 -> 11.2 us, n=512 19.9 -> 17.1 us,
+    // larger shapes unchanged (graph replay, profiles/r01_small_shapes.txt);
+    // LPY_FFMA_MINKB overrides it for A/B runs.
+    static const int min_kb = [] {
+        const char *e = getenv("LPY_FFMA_MINKB");
+        return e ? atoi(e) : 1;
+    }();
+    prm.splits = choose_splits(prm.num_tiles, prm.k_blocks, kn.num_sms, min_kb, MAX_SPLITS);
     prm.num_units = prm.num_tiles * prm.splits;
     prm.ws = nullptr;
     int grid = kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms;
