@@ -323,8 +323,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                             // a_big * b_small, a_big * b_big, a_small * b_big: the two MMAs
                             // sharing A back to back measured 1-3% faster than small terms first
                             // (accuracy unchanged: every partial is promoted within 128 of K)
-                            umma_tf32_cg<CG>(d, a_big, b_big + SMALL, idesc, (first && sub == 0) ? 0u : 1u);
-                            umma_tf32_cg<CG>(d, a_big, b_big, idesc, 1u);
+                            // A_big through the tensor core's collector: read from shared
+                            // memory once for both of its MMAs (fill / lastuse), which
+                            // eases the shared-memory port that bounds the narrow tiles
+                            // (n=1024, BN=128: 27.8 -> 26.9 us; no change at n=8192;
+                            // profiles/r01_tf32_collector.txt)
+                            if constexpr (CG == 2) {
+                                umma_tf32_cg2_coll<ACollector::Fill>(d, a_big, b_big + SMALL, idesc,
+                                                                     (first && sub == 0) ? 0u : 1u);
+                                umma_tf32_cg2_coll<ACollector::LastUse>(d, a_big, b_big, idesc, 1u);
+                            } else {
+                                umma_tf32_cg<CG>(d, a_big, b_big + SMALL, idesc, (first && sub == 0) ? 0u : 1u);
+                                umma_tf32_cg<CG>(d, a_big, b_big, idesc, 1u);
+                            }
                             umma_tf32_cg<CG>(d, a_big + SMALL, b_big, idesc, 1u);
                         }
                         umma_commit_cg<CG>(&empty[s]);

@@ -309,6 +309,24 @@ __device__ __forceinline__ void umma_tf32_cg(uint32_t d_tmem, uint64_t a_desc, u
             "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
             : "memory");
 }
+// As umma_tf32_cg (CG = 2) with an A-operand collector hint: FILL keeps A in
+// the tensor core's collector for the next MMA, LASTUSE reads it from there
+// (and releases it) instead of from shared memory.
+enum class ACollector { Fill, LastUse };
+template <ACollector U>
+__device__ __forceinline__ void umma_tf32_cg2_coll(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                   uint32_t idesc, uint32_t accumulate) {
+    if constexpr (U == ACollector::Fill)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32.collector::a::fill [%0], %1, %2, %3, p;\n\t}"
+            ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}"
+            ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
 // Commit: arrive on `bar` (in both CTAs of the pair for CG = 2) once all MMAs
 // issued so far by this thread have completed.
 template <int CG>

@@ -383,3 +383,18 @@ def test_cuda_graph_capture(path, M, N, K, ld_pad):
         torch.cuda.synchronize()
         assert torch.equal(C, eager)
     check(C.cpu().numpy(), A, B)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("M,N,K", [(1, 4096, 4096), (4096, 1, 4096), (4096, 4096, 1), (3, 5, 65536),
+                                   (64, 64, 65536), (5000, 8, 300)])
+def test_skinny_and_long_k_shapes(path, M, N, K):
+    """Degenerate aspect ratios (no config is skinny, the path
+    must still be right): a row or column vector output (one tile row or
+    column, mostly out-of-bounds TMA boxes), a rank-1 product (K = 1: one
+    partial k-block, nothing to split), and long reductions (K = 65536:
+    split-K with many slices, 512+ promotions of the TMEM partial)."""
+    A, B = inputs(M, N, K, seed=M + N)
+    C, pad_ok = run_gemm(A, B, path=path)
+    assert pad_ok
+    check(C, A, B)
