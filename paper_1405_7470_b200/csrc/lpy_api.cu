@@ -282,45 +282,53 @@ lpy_status lpy_gemm_f32_ex(int64_t M, int64_t N, int64_t K, const float *A, int6
 
     const lpy_path chosen = resolve_path(M, N, K, path);
 
-    // Aligned repack (reading A7) of any operand TMA cannot describe directly.
-    float *scratch[2] = {nullptr, nullptr};
+    // a tile width only the 3xTF32 kernel has: refused before anything is enqueued
+    if (opts && opts->tile_n == 192 && (chosen == LPY_PATH_FFMA || !lpy::tf32_available()))
+        return LPY_ERR_NOT_SUPPORTED;
+
+    // Aligned repack (reading A7) of any operand TMA cannot describe directly:
+    // one stream-ordered scratch allocation and one launch for both operands.
+    lpy::RepackJob jobs[2];
+    int njobs = 0;
+    size_t scratch_floats = 0;
     Operand *ops[2] = {&oa, &ob};
+    int64_t ld2[2] = {0, 0};
+    size_t off[2] = {0, 0};
     for (int i = 0; i < 2; ++i) {
-        Operand &o = *ops[i];
+        const Operand &o = *ops[i];
         if ((reinterpret_cast<uintptr_t>(o.p) & 15) == 0 && (o.ld & 3) == 0) continue;
-        const int64_t ld2 = (o.inner() + 3) & ~int64_t(3);
-        e = cudaMallocAsync(reinterpret_cast<void **>(&scratch[i]), size_t(o.lines() * ld2) * 4, s);
+        ld2[i] = (o.inner() + 3) & ~int64_t(3);
+        off[i] = scratch_floats;
+        scratch_floats += size_t(o.lines() * ld2[i]);
+    }
+    float *scratch = nullptr;
+    if (scratch_floats > 0) {
+        e = cudaMallocAsync(reinterpret_cast<void **>(&scratch), scratch_floats * 4, s);
+        if (e != cudaSuccess) return cuda_fail(e);
+        for (int i = 0; i < 2; ++i) {
+            Operand &o = *ops[i];
+            if (ld2[i] == 0) continue;
+            jobs[njobs++] = lpy::RepackJob{o.p, o.ld, scratch + off[i], ld2[i], o.lines(), o.inner()};
+            o.p = scratch + off[i];
+            o.ld = ld2[i];
+        }
+        e = lpy::launch_repack(jobs, njobs, dev.sms, s);
         if (e != cudaSuccess) {
-            for (int j = 0; j < i; ++j)
-                if (scratch[j]) cudaFreeAsync(scratch[j], s);
+            cudaFreeAsync(scratch, s);
             return cuda_fail(e);
         }
-        e = lpy::launch_repack(o.p, o.ld, scratch[i], ld2, o.lines(), o.inner(), s);
-        if (e != cudaSuccess) {
-            for (int j = 0; j <= i; ++j)
-                if (scratch[j]) cudaFreeAsync(scratch[j], s);
-            return cuda_fail(e);
-        }
-        o.p = scratch[i];
-        o.ld = ld2;
     }
 
     lpy::Problem prob{int(M), int(N), int(K), oa.p, oa.ld, oa.layout, ob.p, ob.ld, ob.layout, C, ldc};
     lpy::Knobs kn{opts ? opts->num_ctas : 0, opts ? opts->raster_group : 0, opts ? opts->promote_kblocks : 0,
                   dev.sms, opts ? opts->tile_n : 0};
-    if (kn.tile_n == 192 && (chosen == LPY_PATH_FFMA || !lpy::tf32_supported(prob))) {
-        for (int i = 0; i < 2; ++i)
-            if (scratch[i]) cudaFreeAsync(scratch[i], s);
-        return LPY_ERR_NOT_SUPPORTED;
-    }
     if (chosen == LPY_PATH_3XTF32 && !lpy::tf32_supported(prob)) {
         st = (path == LPY_PATH_3XTF32) ? LPY_ERR_NOT_SUPPORTED : LPY_OK;
         if (st == LPY_OK) e = lpy::launch_ffma(prob, kn, s);
     } else {
         e = chosen == LPY_PATH_3XTF32 ? lpy::launch_3xtf32(prob, kn, s) : lpy::launch_ffma(prob, kn, s);
     }
-    for (int i = 0; i < 2; ++i)
-        if (scratch[i]) cudaFreeAsync(scratch[i], s);
+    if (scratch) cudaFreeAsync(scratch, s);
     if (st != LPY_OK) return st;
     return e == cudaSuccess ? LPY_OK : cuda_fail(e);
 }

@@ -69,8 +69,14 @@ cudaError_t launch_saxpy(int64_t n, float alpha, const float *x, int64_t incx, f
 cudaError_t launch_coulomb(int64_t nt, const float *t, int64_t ldt, int64_t ns, const float *s, int64_t lds,
                            const float *q, float *phi, int num_sms, cudaStream_t st);
 
-// dst[line*ld_dst + e] = src[line*ld_src + e] for line < lines, e < inner.
-cudaError_t launch_repack(const float *src, int64_t ld_src, float *dst, int64_t ld_dst,
-                          int64_t lines, int64_t inner, cudaStream_t s);
+// dst[line*ld_dst + e] = src[line*ld_src + e] for line < lines, e < inner
+// (pad columns zeroed), for njobs (1 or 2) operands in one launch.
+struct RepackJob {
+    const float *src;
+    int64_t ld_src;
+    float *dst;
+    int64_t ld_dst, lines, inner;
+};
+cudaError_t launch_repack(const RepackJob *jobs, int njobs, int num_sms, cudaStream_t s);
 
 }  // namespace lpy

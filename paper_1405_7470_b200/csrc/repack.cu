@@ -10,28 +10,45 @@ namespace lpy {
 
 // One warp per line (grid-stride over lines): 32 consecutive 4-byte loads and
 // stores per instruction, so even short lines (the ragged config's 777 floats)
-// move at full coalescing; the grid fills every SM once.
-__global__ void __launch_bounds__(256) repack_kernel(const float *__restrict__ src, int64_t ld_src,
-                                                     float *__restrict__ dst, int64_t ld_dst, int64_t lines,
-                                                     int64_t inner) {
+// move at full coalescing, and UNROLL loads in flight per lane before their
+// stores (a load / store chain per element would leave each warp waiting one
+// memory latency per 128 bytes).  The pad columns of dst are zeroed (TMA never
+// reads them: the descriptors carry the logical extent).
+constexpr int REPACK_UNROLL = 16;
+__global__ void __launch_bounds__(256) repack_kernel(RepackJob j0, RepackJob j1, int njobs) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-    for (int64_t line = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); line < lines;
-         line += warps) {
-        const float *s = src + line * ld_src;
-        float *d = dst + line * ld_dst;
-        for (int64_t e = lane; e < ld_dst; e += 32) d[e] = e < inner ? s[e] : 0.f;   // zero the pad
+    const int64_t total = j0.lines + (njobs > 1 ? j1.lines : 0);
+    for (int64_t gl = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); gl < total; gl += warps) {
+        const bool first = gl < j0.lines;
+        const RepackJob &j = first ? j0 : j1;
+        const int64_t line = first ? gl : gl - j0.lines;
+        const float *s = j.src + line * j.ld_src;
+        float *d = j.dst + line * j.ld_dst;
+        for (int64_t e0 = lane; e0 < j.ld_dst; e0 += 32 * REPACK_UNROLL) {
+            float v[REPACK_UNROLL];
+#pragma unroll
+            for (int k = 0; k < REPACK_UNROLL; ++k) {
+                const int64_t e = e0 + 32 * k;
+                v[k] = e < j.inner ? __ldg(s + e) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < REPACK_UNROLL; ++k) {
+                const int64_t e = e0 + 32 * k;
+                if (e < j.ld_dst) d[e] = v[k];
+            }
+        }
     }
 }
 
-cudaError_t launch_repack(const float *src, int64_t ld_src, float *dst, int64_t ld_dst, int64_t lines,
-                          int64_t inner, cudaStream_t s) {
-    if (lines <= 0 || inner <= 0) return cudaSuccess;
-    int dev = 0, sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+// Both operands' repacks (njobs = 1 or 2) in one launch.
+cudaError_t launch_repack(const RepackJob *jobs, int njobs, int num_sms, cudaStream_t s) {
+    int64_t lines = 0;
+    for (int i = 0; i < njobs; ++i) lines += jobs[i].lines;
+    if (njobs <= 0 || lines <= 0) return cudaSuccess;
     int64_t blocks = (lines + 7) / 8;
-    if (blocks > int64_t(sms) * 8) blocks = int64_t(sms) * 8;
-    repack_kernel<<<unsigned(blocks), 256, 0, s>>>(src, ld_src, dst, ld_dst, lines, inner);
+    if (blocks > int64_t(num_sms) * 8) blocks = int64_t(num_sms) * 8;
+    repack_kernel<<<unsigned(blocks), 256, 0, s>>>(jobs[0], njobs > 1 ? jobs[1] : jobs[0], njobs);
     return cudaGetLastError();
 }
 

@@ -38,7 +38,19 @@ def per_call(fn, reps=300):
     return 1e6 * dt / reps
 
 
-rows = [("ctypes no-op (lpy_version)", lambda: lib.lpy_version())]
+probe_path = os.path.join(ROOT, "paper_1405_7470_b200", "liblpy_probe.so")
+rows = [("ctypes no-op (lpy_version)", lambda: lib.lpy_version()),
+        ("C ABI M=0 (validation only)",
+         lambda: lib.lpy_gemm_f32_ex(0, n, n, pa, n, 0, pb, n, 0, pc, n, 0, stream, 0, None)),
+        ("C ABI K=0 (validation + memset)",
+         lambda: lib.lpy_gemm_f32_ex(n, n, 0, pa, n, 0, pb, n, 0, pc, n, 0, stream, 0, None))]
+if os.path.exists(probe_path):
+    import ctypes
+    probe = ctypes.CDLL(probe_path)
+    probe.lpy_probe_empty_launch.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p, ctypes.c_void_p]
+    flag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    rows.append(("empty kernel <<<148, 384, 197 KB>>>",
+                 lambda: probe.lpy_probe_empty_launch(148, 384, 197 << 10, flag.data_ptr(), stream)))
 for path in ("ffma", "3xtf32"):
     pid = lpy.PATHS[path]
     rows.append((f"C ABI lpy_gemm_f32_ex {path}",
