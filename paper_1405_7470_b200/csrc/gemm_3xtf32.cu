@@ -37,6 +37,7 @@
 // Operand smem layouts: K-major tiles use the 64B swizzle (16 fp32 per row);
 // MN-major tf32 tiles must use SWIZZLE_128B_BASE32B (TMA "128B_ATOM_32B").
 #include <cstdlib>
+#include <mutex>
 #include "lpy_internal.h"
 #include "ptx.cuh"
 
@@ -78,6 +79,10 @@ struct Params {
     // of short units fills all CTA pairs.  Slice partials are parked in `ws` and
     // the slice that finishes a tile last adds them in slice order.
     int full_tiles, splits, num_units;
+    // cluster split (a single under-filled wave): every tile is cut into
+    // `splits` k-slices computed by the `splits` CTA pairs of one cluster, whose
+    // partials are summed through distributed shared memory (no ws / sem)
+    int cluster_split;
     float *ws;          // [(num_units - full_tiles)][CG][BM x BN] partial tiles
     int *sem;           // [(num_tiles - full_tiles)][CG] arrival counters, zero on entry and exit
 };
@@ -175,9 +180,9 @@ __device__ __forceinline__ void store_row8(const Params &p, float *crow, int col
 
 // Arrive (one per warp) on the leader CTA's copy of `bar`.
 template <int CG>
-__device__ __forceinline__ void arrive_leader(uint64_t *bar) {
+__device__ __forceinline__ void arrive_leader(uint64_t *bar, uint32_t lead) {
     if constexpr (CG == 1) mbar_arrive(bar);
-    else                   mbar_arrive_remote(mapa_shared(smem_u32(bar), 0));
+    else                   mbar_arrive_remote(mapa_shared(smem_u32(bar), lead));
 }
 
 template <int CG, bool AMN, bool BMN, int BN>
@@ -187,6 +192,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     using C_ = Cfg<CG, BN>;
     constexpr int EC = C_::EC;
     constexpr int STAGES = C_::STAGES;
+    static_assert(size_t(BM) * (BN + 4) * 4 <= size_t(STAGES) * C_::STAGE_BYTES,
+                  "cluster-split staging must fit in the operand ring");
     constexpr uint32_t A_BYTES = C_::A_BYTES, RAW_BYTES = C_::RAW_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
 
     extern __shared__ uint8_t smem_raw[];
@@ -202,7 +209,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int rank = CG == 2 ? int(cluster_ctarank()) : 0;
+    // rank: which CTA of the pair (0 = the MMA-issuing leader); lead: the
+    // leader's rank in the cluster (pairs are ranks (2q, 2q+1); a cluster
+    // holds one pair, or `splits` pairs in a cluster split)
+    const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;
+    const int rank = int(crank & 1);
+    const uint32_t lead = crank & ~1u;
+    const uint16_t pair_mask = uint16_t(3u << lead);
     const int unit0 = blockIdx.x / CG, units = gridDim.x / CG;   // this pair's first tile, stride
 
     if (threadIdx.x == 0) {
@@ -338,8 +351,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                             }
                             umma_tf32_cg<CG>(d, a_big + SMALL, b_big, idesc, 1u);
                         }
-                        umma_commit_cg<CG>(&empty[s]);
-                        if (last) umma_commit_cg<CG>(&accf[b]);
+                        umma_commit_cg<CG>(&empty[s], pair_mask);
+                        if (last) umma_commit_cg<CG>(&accf[b], pair_mask);
                         TL(5);
                     }
                     __syncwarp();
@@ -378,7 +391,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) arrive_leader<CG>(&ready[s]);
+                if (lane == 0) arrive_leader<CG>(&ready[s], lead);
                 if (++s == STAGES) { s = 0; ph ^= 1; }
                 TR_ADD(6, t_x);
             }
@@ -422,7 +435,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) arrive_leader<CG>(&acce[b]);
+                if (lane == 0) arrive_leader<CG>(&acce[b], lead);
                 TR_ADD(7, t_b);
             }
             // one row per thread (TMEM lane = row), written with 32-byte stores so
@@ -440,6 +453,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tile_coords(t, p, tm, tn);
                 return tn * BN + half * EC;
             };
+            if (p.cluster_split) {
+                // cluster split: park this slice's partial in this CTA's own shared
+                // memory (the operand ring is idle: the accf commit covers every MMA
+                // of the pair, so nothing reads it any more); rows padded by 4
+                // floats so a warp's float4 stores (32 rows) hit distinct banks.
+                // Summed across the cluster's slices after the cluster barrier.
+                float *dst = reinterpret_cast<float *>(stages) + (quad * 32 + lane) * (BN + 4) + half * EC;
+#pragma unroll
+                for (int j = 0; j < EC; j += 4)
+                    *reinterpret_cast<float4 *>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                continue;
+            }
             if (su >= 0) {
                 // split tile: park this slice's partial as thread-interleaved
                 // 32-byte vectors (a warp writes 1 KB contiguous), count arrivals
@@ -499,6 +524,53 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
 
     if (threadIdx.x == EPI_WARP0 * 32) TL(7);
+    if constexpr (CG == 2) {
+        if (p.cluster_split) {
+            // every slice's partial parked (all threads of the cluster arrive)
+            cluster_sync();
+            if (warp >= EPI_WARP0) {
+                // This CTA sums rows [q*RPS, (q+1)*RPS) of its half of the tile
+                // (q = its pair's slice) over the cluster's slices in slice order,
+                // reading each slice's partial from the same half's CTA through
+                // distributed shared memory, and stores them to C coalesced
+                // (consecutive threads take consecutive float4s of a row).
+                const int ks = p.splits;
+                const int q = unit0 % ks, t = unit0 / ks;
+                int tm, tn;
+                tile_coords(t, p, tm, tn);
+                const int rps = BM / ks;
+                const int row0 = tm * (BM * CG) + rank * BM;
+                const int col0 = tn * BN;
+                const uint32_t stg = smem_u32(stages);
+                constexpr int C4 = BN / 4;
+                const int items = rps * C4;
+#pragma unroll 4
+                for (int idx = threadIdx.x - EPI_WARP0 * 32; idx < items; idx += EPI_WARPS * 32) {
+                    const int rl = q * rps + idx / C4, c4 = idx % C4;
+                    const uint32_t off = stg + uint32_t((rl * (BN + 4) + c4 * 4) * 4);
+                    float4 v[MAX_SPLITS];
+#pragma unroll
+                    for (int sl = 0; sl < MAX_SPLITS; ++sl)
+                        if (sl < ks) v[sl] = ld_dsmem_v4(mapa_shared(off, uint32_t(2 * sl + rank)));
+#pragma unroll
+                    for (int sl = 1; sl < MAX_SPLITS; ++sl)
+                        if (sl < ks) { v[0].x += v[sl].x; v[0].y += v[sl].y; v[0].z += v[sl].z; v[0].w += v[sl].w; }
+                    const int row = row0 + rl, col = col0 + c4 * 4;
+                    if (row < p.M) {
+                        float *c = p.C + int64_t(row) * p.ldc + col;
+                        if (p.c_vec && col + 3 < p.N) {
+                            *reinterpret_cast<float4 *>(c) = v[0];
+                        } else {
+                            const float o[4] = {v[0].x, v[0].y, v[0].z, v[0].w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                if (col + e < p.N) c[e] = o[e];
+                        }
+                    }
+                }
+            }
+        }
+    }
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     if (warp == 1) tmem_dealloc_cg<CG>(tmem, TMEM_COLS);
@@ -520,7 +592,7 @@ static cudaError_t launch_t(const CUtensorMap &ta, const CUtensorMap &tb, const 
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.x = CG * (prm.cluster_split ? prm.splits : 1);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -535,20 +607,25 @@ static long long *g_trace = nullptr;   // set by lpy_trace_set_buffer (diagnosti
 //  * >= 2 waves with a partial last one: its `rem` tiles are cut into
 //    S = floor(pairs / rem) slices (<= 4, >= 16 k-blocks each), so the last
 //    wave is S times shorter;
-//  * a single under-filled wave (tiles < pairs, e.g. n = 1024) is NOT split by
-//    default: cutting every tile into S = floor(pairs / tiles) slices fills the
-//    CTA pairs, but the last arriver's fix-up (S partials of 128 KB read by one
-//    SM at ~50 GB/s, then the tile stored) costs more than the k-loop saves --
-//    measured at n = 1024: 28.2 us unsplit (BN = 128) vs 32.9-38.8 us split
-//    S = 4 (BN = 256) in graph replay (profiles/r01_tf32_split1.txt).
-//    LPY_TF32_SPLIT1=1 enables it (diagnostics / A-B).
-struct TailSplit { int splits, full_tiles, num_units; };
-static TailSplit tail_split(int num_tiles, int k_blocks, int pairs) {
+//  * a single under-filled wave (tiles < pairs, e.g. n = 1024): every tile is
+//    cut into S = 2 or 4 k-slices (S * tiles <= pairs, >= 8 k-blocks each)
+//    computed by the S CTA pairs of one cluster (2S CTAs), which sum their
+//    partials through distributed shared memory, each CTA reducing and
+//    storing 1/S of its rows (`cluster_split`).  The global-memory variant of
+//    this split (last arriver re-reads S partials of 128 KB through one SM at
+//    ~50 GB/s) was slower than no split (profiles/r01_tf32_split1.txt); the
+//    cluster's barrier is safe where a global spin-wait is not, since the
+//    hardware co-schedules a cluster's CTAs.  LPY_TF32_SPLIT1=0 disables it.
+//    S = 4 needs clusters of 8 CTAs, of which only `caps.max8` fit on the chip
+//    at once (a cluster lives in one GPC), so S follows what fits in one wave.
+struct ClusterCaps { int max4, max8; };   // co-resident clusters of 4 / 8 CTAs
+struct TailSplit { int splits, full_tiles, num_units, cluster; };
+static TailSplit tail_split(int num_tiles, int k_blocks, int pairs, const ClusterCaps &caps) {
     static const bool split1 = [] {
         const char *e = getenv("LPY_TF32_SPLIT1");
-        return e && e[0] == '1';
+        return !(e && e[0] == '0');
     }();
-    TailSplit r{1, num_tiles, num_tiles};
+    TailSplit r{1, num_tiles, num_tiles, 0};
     if (num_tiles <= 0 || pairs <= 0) return r;
     const int waves = (num_tiles + pairs - 1) / pairs;
     const int rem = num_tiles - (waves - 1) * pairs;
@@ -556,7 +633,18 @@ static TailSplit tail_split(int num_tiles, int k_blocks, int pairs) {
     if (S > MAX_SPLITS) S = MAX_SPLITS;
     const int min_kb = waves >= 2 ? 16 : 8;
     while (S > 1 && k_blocks / S < min_kb) --S;
-    if (S < 2 || (waves < 2 && !split1)) return r;
+    if (waves < 2) {
+        if (S == 3) S = 2;   // clusters of 2S CTAs: 4 or 8
+        if (S == 4 && num_tiles > caps.max8) S = 2;
+        if (S == 2 && num_tiles > caps.max4) S = 1;
+        if (S < 2 || !split1) return r;
+        r.splits = S;
+        r.full_tiles = 0;
+        r.num_units = num_tiles * S;
+        r.cluster = 1;
+        return r;
+    }
+    if (S < 2) return r;
     r.splits = S;
     r.full_tiles = (waves - 1) * pairs;
     r.num_units = r.full_tiles + (num_tiles - r.full_tiles) * S;
@@ -572,12 +660,12 @@ static TailSplit tail_split(int num_tiles, int k_blocks, int pairs) {
 // over the useful columns; narrower wins only by > 3%.  n >= 4096 -> 256;
 // n = 1024 -> 128 (32 tiles instead of 16); the ragged config -> 192 (64 tiles
 // instead of 48).
-int choose_bn(int M, int N, int K, int pairs) {
+int choose_bn(int M, int N, int K, int pairs, const ClusterCaps &caps) {
     const int64_t tm = (M + 2 * BM - 1) / (2 * BM);
     const int kb = (K + BK - 1) / BK;
     auto cost = [&](int bn) {
         const int64_t tn = (N + bn - 1) / bn, tiles = tm * tn;
-        const TailSplit ts = tail_split(int(tiles), kb, pairs);
+        const TailSplit ts = tail_split(int(tiles), kb, pairs, caps);
         const double kern = bn == 256 ? 1.0 : bn == 192 ? 0.86 : 0.69;
         // whole-tile waves, then the split units' waves at 1/S of a tile each
         const int64_t full_waves = (ts.full_tiles + pairs - 1) / pairs;
@@ -593,7 +681,7 @@ int choose_bn(int M, int N, int K, int pairs) {
 }
 
 template <int CG, int BN>
-static cudaError_t launch_cg(const Problem &p, const Knobs &kn, cudaStream_t s) {
+static cudaError_t launch_cg(const Problem &p, const Knobs &kn, const ClusterCaps &caps, cudaStream_t s) {
     const bool AMN = (p.la == 1);   // column-major A: M contiguous
     const bool BMN = (p.lb == 0);   // row-major B: N contiguous
     constexpr int BN_CTA = Cfg<CG, BN>::BN_CTA;
@@ -624,18 +712,26 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, cudaStream_t s) 
     prm.l2hint = l2hint;
     prm.trace = g_trace;
     {
-        const TailSplit ts = tail_split(prm.num_tiles, prm.k_blocks, kn.num_sms / CG);
+        const TailSplit ts = tail_split(prm.num_tiles, prm.k_blocks, kn.num_sms / CG, caps);
         prm.splits = ts.splits;
         prm.full_tiles = ts.full_tiles;
         prm.num_units = ts.num_units;
+        prm.cluster_split = CG == 2 ? ts.cluster : 0;
+        if (CG == 1 && ts.cluster) {   // (single-CTA diagnostics variant: no cluster split)
+            prm.splits = 1;
+            prm.full_tiles = prm.num_units = prm.num_tiles;
+        }
     }
     prm.ws = nullptr;
     prm.sem = nullptr;
     int units = (kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms) / CG;  // CTAs (pairs) in the grid
     if (units > prm.num_units) units = prm.num_units;
     if (units < 1) units = 1;
+    // cluster split: one cluster per tile, every pair runs exactly one unit
+    // (opts.num_ctas cannot shrink this grid; results do not depend on it)
+    if (prm.cluster_split) units = prm.num_units;
     const int grid = units * CG;
-    if (prm.splits > 1) {
+    if (prm.splits > 1 && !prm.cluster_split) {
         const int split_tiles = prm.num_tiles - prm.full_tiles;
         const size_t ws_bytes = size_t(split_tiles) * prm.splits * CG * BM * BN * 4;
         char *buf = nullptr;
@@ -647,12 +743,66 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, cudaStream_t s) 
         if (e != cudaSuccess) { cudaFreeAsync(buf, s); return e; }
     }
 
-    if (AMN && BMN)       e = launch_t<CG, true, true, BN>(ta, tb, prm, grid, s);
-    else if (AMN && !BMN) e = launch_t<CG, true, false, BN>(ta, tb, prm, grid, s);
-    else if (!AMN && BMN) e = launch_t<CG, false, true, BN>(ta, tb, prm, grid, s);
-    else                  e = launch_t<CG, false, false, BN>(ta, tb, prm, grid, s);
+    auto launch = [&](const Params &q, int g) {
+        if (AMN && BMN)  return launch_t<CG, true, true, BN>(ta, tb, q, g, s);
+        if (AMN && !BMN) return launch_t<CG, true, false, BN>(ta, tb, q, g, s);
+        if (!AMN && BMN) return launch_t<CG, false, true, BN>(ta, tb, q, g, s);
+        return launch_t<CG, false, false, BN>(ta, tb, q, g, s);
+    };
+    e = launch(prm, grid);
+    if (e != cudaSuccess && prm.cluster_split) {
+        // a cluster of 2S CTAs this size could not be placed (configuration
+        // error, nothing enqueued): run the tiles whole instead
+        (void)cudaGetLastError();
+        Params q = prm;
+        q.cluster_split = 0;
+        q.splits = 1;
+        q.full_tiles = q.num_units = q.num_tiles;
+        const int g = CG * (q.num_units < kn.num_sms / CG ? q.num_units : kn.num_sms / CG);
+        e = launch(q, g > 0 ? g : CG);
+    }
     if (prm.ws) cudaFreeAsync(prm.ws, s);
     return e;
+}
+
+// Co-resident clusters of 4 and 8 CTAs of the (one CTA per SM) kernel on the
+// current device, queried once per device.
+static ClusterCaps cluster_caps(int num_sms) {
+    static std::mutex mu;
+    static ClusterCaps cache[64];
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return ClusterCaps{0, 0};
+    std::lock_guard<std::mutex> g(mu);
+    if (done[dev]) return cache[dev];
+    using C_ = Cfg<2, 256>;
+    auto kern = gemm_3xtf32_kernel<2, false, true, 256>;
+    static std::atomic<uint64_t> attr_done{0};
+    ClusterCaps c{0, 0};
+    if (ensure_smem_attr(kern, int(C_::SMEM_BYTES), attr_done) == cudaSuccess) {
+        for (int size : {4, 8}) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(size * (num_sms / size > 0 ? num_sms / size : 1));
+            cfg.blockDim = dim3(THREADS);
+            cfg.dynamicSmemBytes = C_::SMEM_BYTES;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = size;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+                (void)cudaGetLastError();
+                n = 0;
+            }
+            (size == 4 ? c.max4 : c.max8) = n;
+        }
+    }
+    cache[dev] = c;
+    done[dev] = true;
+    return c;
 }
 
 }  // namespace tf32
@@ -666,7 +816,8 @@ cudaError_t launch_3xtf32(const Problem &p, const Knobs &kn, cudaStream_t s) {
         const char *e = getenv("LPY_TF32_CG");
         return (e && e[0] == '1') ? 1 : 2;
     }();
-    if (cg == 1) return tf32::launch_cg<1, 256>(p, kn, s);
+    const tf32::ClusterCaps caps = tf32::cluster_caps(kn.num_sms);
+    if (cg == 1) return tf32::launch_cg<1, 256>(p, kn, caps, s);
     // LPY_TF32_BN=128|192|256 forces the tile width (diagnostics / A-B comparison).
     static const int force_bn = [] {
         const char *e = getenv("LPY_TF32_BN");
@@ -677,11 +828,11 @@ cudaError_t launch_3xtf32(const Problem &p, const Knobs &kn, cudaStream_t s) {
     // or from opts.tile_n (dist.py's per-chunk products, which share the GPU,
     // ask for full-width tiles)
     const int pairs = kn.num_sms / 2;
-    const int bn = kn.tile_n ? kn.tile_n : force_bn ? force_bn : tf32::choose_bn(p.M, p.N, p.K, pairs > 0 ? pairs : 1);
+    const int bn = kn.tile_n ? kn.tile_n : force_bn ? force_bn : tf32::choose_bn(p.M, p.N, p.K, pairs > 0 ? pairs : 1, caps);
     switch (bn) {
-        case 128: return tf32::launch_cg<2, 128>(p, kn, s);
-        case 192: return tf32::launch_cg<2, 192>(p, kn, s);
-        default:  return tf32::launch_cg<2, 256>(p, kn, s);
+        case 128: return tf32::launch_cg<2, 128>(p, kn, caps, s);
+        case 192: return tf32::launch_cg<2, 192>(p, kn, caps, s);
+        default:  return tf32::launch_cg<2, 256>(p, kn, caps, s);
     }
 }
 

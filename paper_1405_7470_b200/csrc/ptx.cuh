@@ -329,15 +329,25 @@ __device__ __forceinline__ void umma_tf32_cg2_coll(uint32_t d_tmem, uint64_t a_d
 }
 // Commit: arrive on `bar` (in both CTAs of the pair for CG = 2) once all MMAs
 // issued so far by this thread have completed.
+// `pair_mask`: the two CTAs of the pair in the cluster (0b11 << first rank).
 template <int CG>
-__device__ __forceinline__ void umma_commit_cg(uint64_t *bar) {
+__device__ __forceinline__ void umma_commit_cg(uint64_t *bar, uint16_t pair_mask = 3) {
     if constexpr (CG == 1) umma_commit(bar);
     else
         asm volatile(
             "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
             " [%0], %1;" ::"r"(smem_u32(bar)),
-            "h"(uint16_t(3))
+            "h"(pair_mask)
             : "memory");
+}
+// 16 bytes from a shared::cluster address (another CTA's shared memory).
+__device__ __forceinline__ float4 ld_dsmem_v4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
 }
 
 // Each thread of the warp reads 16 consecutive 32-bit columns of its TMEM lane.

@@ -36,12 +36,14 @@ for path in ("ffma", "3xtf32"):
     worst = max(worst, check(C, A, B))
 print(f"sanitize_small: all products within tolerance (worst {worst:.2e})")
 
-# split-K FFMA (under-filled grid: 72 tiles -> 2 slices) and the 3xTF32 tail
-# split (90 pair tiles = 2 waves, the last 16 cut into k-slices)
+# split-K FFMA (under-filled grid: 72 tiles -> 2 slices), the 3xTF32 tail
+# split (90 pair tiles = 2 waves, the last 16 cut into k-slices) and the 3xTF32
+# cluster split (single under-filled waves: k-slices summed through DSMEM)
 import paper_1405_7470_b200 as lpy  # noqa: E402
 import oracle  # noqa: E402
 import torch  # noqa: E402
-for path, (M, N, K) in (("ffma", (1000, 1100, 600)), ("3xtf32", (2560, 2304, 1024))):
+for path, (M, N, K) in (("ffma", (1000, 1100, 600)), ("3xtf32", (2560, 2304, 1024)),
+                        ("3xtf32", (512, 512, 512)), ("3xtf32", (1024, 1024, 1024)), ("3xtf32", (700, 600, 520))):
     A = synth.matrix(M, K, seed=5, matrix_id=0)
     B = synth.matrix(K, N, seed=5, matrix_id=1)
     C, pad_ok = run_gemm(A, B, 0, 0, 0, path=path)
