@@ -45,6 +45,7 @@ constexpr int BM = 128, BK = 32;             // tile width BN: template (128 or 
 constexpr int KSUB = 32;                     // k per 128B-swizzled K-major TMA box (= BK)
 constexpr int CWARPS = 8;                    // consumer warps: 2 along m (64 rows) x 4 along n (BN/4 cols)
 constexpr int XWARPS = 3;                    // transpose warps (warps CWARPS+1 .. CWARPS+3)
+constexpr int MAX_SPLITS = 8;                // split-K slices at most (choose_splits' cap; cluster size)
 
 // Per-layout geometry.  AK: A is K-major (row-major A); BKM: B is K-major
 // (column-major B).  Each stage holds the raw TMA tiles plus MN-major copies
@@ -78,7 +79,11 @@ struct Params {
     // split-K (bulk/edge specialisation for under-filled grids): work unit
     // u = tile * splits + slice covers k-blocks [slice*KB/splits, (slice+1)*KB/splits)
     int splits, num_units;
-    float *ws;       // [num_units][BM*BN] partial tiles (splits > 1)
+    float *ws;       // [num_units][BM*BN] partial tiles (splits > 1, not cluster_split)
+    // cluster split (a single wave, splits <= 8): the `splits` CTAs of one
+    // cluster compute the slices of one tile and sum them through distributed
+    // shared memory (no ws, no fix-up kernel)
+    int cluster_split;
 };
 
 __device__ __forceinline__ void unit_range(int u, const Params &p, int &t, int &kb0, int &kb1) {
@@ -251,6 +256,10 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
                 }
             }
         }
+        if (SPLIT && p.cluster_split) {   // the consumers' two cluster barriers
+            cluster_sync();
+            cluster_sync();
+        }
         return;
     }
 
@@ -294,6 +303,58 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
 
+        if (SPLIT && p.cluster_split) {
+            // ---------------------------------------- cluster split: DSMEM sum
+            // Park the partial in this CTA's operand ring (idle once every
+            // consumer has read its last stage: one unit per CTA, no more TMA),
+            // rows padded by 4 floats; after a cluster barrier CTA r of the
+            // cluster sums rows [r*BM/S, (r+1)*BM/S) over the S slices in slice
+            // order -- the fix-up kernel's order, so results are bitwise those of
+            // the global-memory split -- and stores them coalesced.
+            named_bar_sync(1, CWARPS * 32);
+            constexpr int LDS_ = BN + 4;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int jp = 0; jp < JN; jp += 2) {
+                    float lo0, hi0, lo1, hi1;
+                    unpack2(acc2[i][jp], lo0, hi0);
+                    unpack2(acc2[i][jp + 1], lo1, hi1);
+                    *reinterpret_cast<float4 *>(stages + a_row(wm, lm, i) * LDS_ + b_col<JN>(wn, ln, 2 * jp)) =
+                        make_float4(lo0, hi0, lo1, hi1);
+                }
+            cluster_sync();
+            const int S = p.splits, r = int(cluster_ctarank());
+            const int r0 = r * BM / S, r1 = (r + 1) * BM / S;
+            constexpr int C4 = BN / 4;
+            const int m0 = tm * BM, n0 = tn * BN;
+            const uint32_t stg = smem_u32(stages);
+            for (int idx = threadIdx.x; idx < (r1 - r0) * C4; idx += CWARPS * 32) {
+                const int rl = r0 + idx / C4, c4 = idx % C4;
+                const uint32_t off = stg + uint32_t((rl * LDS_ + c4 * 4) * 4);
+                float4 v[MAX_SPLITS];
+#pragma unroll
+                for (int sl = 0; sl < MAX_SPLITS; ++sl)
+                    if (sl < S) v[sl] = ld_dsmem_v4(mapa_shared(off, uint32_t(sl)));
+#pragma unroll
+                for (int sl = 1; sl < MAX_SPLITS; ++sl)
+                    if (sl < S) { v[0].x += v[sl].x; v[0].y += v[sl].y; v[0].z += v[sl].z; v[0].w += v[sl].w; }
+                const int row = m0 + rl, col = n0 + c4 * 4;
+                if (row < p.M) {
+                    float *c = p.C + int64_t(row) * p.ldc + col;
+                    if (p.c_vec && col + 3 < p.N) {
+                        *reinterpret_cast<float4 *>(c) = v[0];
+                    } else {
+                        const float o[4] = {v[0].x, v[0].y, v[0].z, v[0].w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (col + e < p.N) c[e] = o[e];
+                    }
+                }
+            }
+            cluster_sync();   // peers done reading this CTA's partial
+            continue;
+        }
         if constexpr (SPLIT) {
             // ---------------------------------------- split-K: park the partial
             // Every slice stores its partial tile (each thread its own 8 x 2JN
@@ -348,7 +409,6 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
 // SM pulls only ~50 GB/s of partials from L2 (bytes in flight / latency), so
 // the fix-up is spread over more SMs than there are tiles.
 constexpr int FIXUP_PARTS = 4;
-constexpr int MAX_SPLITS = 8;     // choose_splits' cap for this path
 template <int BN>
 __global__ void __launch_bounds__(CWARPS * 32) splitk_fixup_kernel(const Params p) {
     constexpr int JN = BN / 32, PER = 8 * JN / 2;
@@ -432,6 +492,61 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     int grid = kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms;
     if (grid > prm.num_units) grid = prm.num_units;
     if (grid < 1) grid = 1;
+    auto kern = prm.splits > 1 ? gemm_ffma_kernel<AK, BKM, BN, true> : gemm_ffma_kernel<AK, BKM, BN, false>;
+    static std::atomic<uint64_t> attr_done[2];
+    e = ensure_smem_attr(kern, int(G::SMEM_BYTES), attr_done[prm.splits > 1]);
+    if (e != cudaSuccess) return e;
+    // Cluster split: a single wave (one unit per CTA), S <= 8 (the portable
+    // cluster size), as many tiles as clusters of S fit at once -> one cluster
+    // per tile, slices summed
+    // through DSMEM (no scratch, no fix-up launch).  LPY_FFMA_CLUSTER=0 keeps the
+    // global-memory split (A/B).
+    static const bool cluster_on = [] {
+        const char *v = getenv("LPY_FFMA_CLUSTER");
+        return !(v && v[0] == '0');
+    }();
+    prm.cluster_split = 0;
+    if (cluster_on && prm.splits >= 2 && prm.splits <= MAX_SPLITS && prm.num_units <= kn.num_sms &&
+        (kn.num_ctas == 0 || kn.num_ctas >= prm.num_units)) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(prm.num_units);
+        cfg.blockDim = dim3(G::THREADS);
+        cfg.dynamicSmemBytes = G::SMEM_BYTES;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = prm.splits;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        // co-resident clusters of this size, once per (kernel variant, device)
+        static std::atomic<int> fit_cache[64][MAX_SPLITS];
+        static std::atomic<bool> fit_init{false};
+        if (!fit_init.load()) {
+            for (auto &d : fit_cache)
+                for (auto &x : d) x.store(-1);
+            fit_init.store(true);
+        }
+        int dev = 0;
+        (void)cudaGetDevice(&dev);
+        std::atomic<int> &slot = fit_cache[dev & 63][prm.splits - 1];
+        int fit = slot.load();
+        if (fit < 0) {
+            if (cudaOccupancyMaxActiveClusters(&fit, kern, &cfg) != cudaSuccess) {
+                (void)cudaGetLastError();
+                fit = 0;
+            }
+            slot.store(fit);
+        }
+        if (fit >= prm.num_tiles) {
+            prm.cluster_split = 1;
+            e = cudaLaunchKernelEx(&cfg, kern, ta, tb, prm);
+            if (e == cudaSuccess) return cudaSuccess;
+            (void)cudaGetLastError();   // not placed: fall back to the global-memory split
+            prm.cluster_split = 0;
+        }
+    }
     if (prm.splits > 1) {
         // The split is fixed by the shape and the device's SM count (never by
         // opts.num_ctas), so results stay bitwise grid-invariant.  Scratch
@@ -441,13 +556,6 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
         if (e != cudaSuccess) return e;
     }
 
-    auto kern = prm.splits > 1 ? gemm_ffma_kernel<AK, BKM, BN, true> : gemm_ffma_kernel<AK, BKM, BN, false>;
-    static std::atomic<uint64_t> attr_done[2];
-    e = ensure_smem_attr(kern, int(G::SMEM_BYTES), attr_done[prm.splits > 1]);
-    if (e != cudaSuccess) {
-        if (prm.ws) cudaFreeAsync(prm.ws, s);
-        return e;
-    }
     kern<<<grid, G::THREADS, G::SMEM_BYTES, s>>>(ta, tb, prm);
     e = cudaGetLastError();
     if (e == cudaSuccess && prm.splits > 1) {
