@@ -42,7 +42,8 @@ print(f"sanitize_small: all products within tolerance (worst {worst:.2e})")
 import paper_1405_7470_b200 as lpy  # noqa: E402
 import oracle  # noqa: E402
 import torch  # noqa: E402
-for path, (M, N, K) in (("ffma", (1000, 1100, 600)), ("3xtf32", (2560, 2304, 1024)),
+for path, (M, N, K) in (("ffma", (1000, 1100, 600)), ("ffma", (1024, 1024, 1024)), ("ffma", (128, 128, 128)),
+                        ("3xtf32", (2560, 2304, 1024)),
                         ("3xtf32", (512, 512, 512)), ("3xtf32", (1024, 1024, 1024)), ("3xtf32", (700, 600, 520))):
     A = synth.matrix(M, K, seed=5, matrix_id=0)
     B = synth.matrix(K, N, seed=5, matrix_id=1)
