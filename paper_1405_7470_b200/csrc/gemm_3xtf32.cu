@@ -71,7 +71,7 @@ struct Params {
     int64_t ldc;
     int tiles_m, tiles_n, num_tiles, k_blocks, group, promote;
     int c_vec;          // C rows 16-byte aligned (float4 stores)
-    int l2hint;         // 0: no L2 hints; 1: A evict_last, B evict_first; 2: the reverse
+    int l2hint;         // 0: no L2 hints; 1-5: eviction-priority experiments (LPY_L2HINT)
     int c_vec8;         // C rows 32-byte aligned (STG.256)
     long long *trace;   // diagnostics build only (-DLPY_TRACE): per-CTA cycle counters
     // Tail split (the ragged last wave): tiles [0, full_tiles) are one work unit
@@ -252,8 +252,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (lane == 0) {
                 tma_prefetch_desc(&tmA);
                 tma_prefetch_desc(&tmB);
-                const uint64_t pol_a = p.l2hint == 1 ? l2_policy_evict_last() : l2_policy_evict_first();
-                const uint64_t pol_b = p.l2hint == 1 ? l2_policy_evict_first() : l2_policy_evict_last();
+                // 1: A last / B first; 2: the reverse; 3: A last / B normal;
+                // 4: B last / A normal; 5: half of A's lines evict_last
+                const uint64_t pol_a = p.l2hint == 1 || p.l2hint == 3 ? l2_policy_evict_last()
+                                       : p.l2hint == 2               ? l2_policy_evict_first()
+                                       : p.l2hint == 5               ? l2_policy_evict_last_frac(0.5f)
+                                                                     : l2_policy_evict_normal();
+                const uint64_t pol_b = p.l2hint == 1 ? l2_policy_evict_first()
+                                       : p.l2hint == 2 || p.l2hint == 4 ? l2_policy_evict_last()
+                                                                        : l2_policy_evict_normal();
                 auto load = [&](void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1, uint64_t pol) {
                     if (p.l2hint) tma_load_2d_hint(dst, tm, bar, c0, c1, pol);
                     else          tma_load_2d(dst, tm, bar, c0, c1);
