@@ -505,22 +505,23 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
         const char *v = getenv("LPY_FFMA_CLUSTER");
         return !(v && v[0] == '0');
     }();
-    prm.cluster_split = 0;
-    if (cluster_on && prm.splits >= 2 && prm.splits <= MAX_SPLITS && prm.num_units <= kn.num_sms &&
-        (kn.num_ctas == 0 || kn.num_ctas >= prm.num_units)) {
+    auto cluster_cfg = [&](int S, cudaLaunchAttribute *attr) {
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(prm.num_units);
+        cfg.gridDim = dim3(prm.num_tiles * S);
         cfg.blockDim = dim3(G::THREADS);
         cfg.dynamicSmemBytes = G::SMEM_BYTES;
         cfg.stream = s;
-        cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = prm.splits;
+        attr[0].val.clusterDim.x = S;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        // co-resident clusters of this size, once per (kernel variant, device)
+        return cfg;
+    };
+    // co-resident clusters of S CTAs, once per (kernel variant, device, S)
+    auto fits = [&](int S) {
+        if (S < 2 || S > MAX_SPLITS || int64_t(prm.num_tiles) * S > kn.num_sms) return false;
         static std::atomic<int> fit_cache[64][MAX_SPLITS];
         static std::atomic<bool> fit_init{false};
         if (!fit_init.load()) {
@@ -530,22 +531,38 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
         }
         int dev = 0;
         (void)cudaGetDevice(&dev);
-        std::atomic<int> &slot = fit_cache[dev & 63][prm.splits - 1];
+        std::atomic<int> &slot = fit_cache[dev & 63][S - 1];
         int fit = slot.load();
         if (fit < 0) {
+            cudaLaunchAttribute attr[1];
+            const cudaLaunchConfig_t cfg = cluster_cfg(S, attr);
             if (cudaOccupancyMaxActiveClusters(&fit, kern, &cfg) != cudaSuccess) {
                 (void)cudaGetLastError();
                 fit = 0;
             }
             slot.store(fit);
         }
-        if (fit >= prm.num_tiles) {
-            prm.cluster_split = 1;
-            e = cudaLaunchKernelEx(&cfg, kern, ta, tb, prm);
-            if (e == cudaSuccess) return cudaSuccess;
-            (void)cudaGetLastError();   // not placed: fall back to the global-memory split
-            prm.cluster_split = 0;
-        }
+        return fit >= prm.num_tiles;
+    };
+    // The split factor, from the shape and the device only (results never depend
+    // on opts.num_ctas): choose_splits' S, or S/2 when clusters of S do not fit at
+    // once but clusters of S/2 do (n = 512: 16 tiles, S = 8 -> 4).
+    bool cluster = cluster_on && fits(prm.splits);
+    if (cluster_on && !cluster && prm.splits >= 4 && fits(prm.splits / 2)) {
+        prm.splits /= 2;
+        prm.num_units = prm.num_tiles * prm.splits;
+        grid = kn.num_ctas > 0 && kn.num_ctas < prm.num_units ? kn.num_ctas : prm.num_units;
+        cluster = true;
+    }
+    prm.cluster_split = 0;
+    if (cluster && (kn.num_ctas == 0 || kn.num_ctas >= prm.num_units)) {
+        cudaLaunchAttribute attr[1];
+        const cudaLaunchConfig_t cfg = cluster_cfg(prm.splits, attr);
+        prm.cluster_split = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, ta, tb, prm);
+        if (e == cudaSuccess) return cudaSuccess;
+        (void)cudaGetLastError();   // not placed: the same split through global memory
+        prm.cluster_split = 0;
     }
     if (prm.splits > 1) {
         // The split is fixed by the shape and the device's SM count (never by
