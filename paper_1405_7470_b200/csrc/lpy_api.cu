@@ -3,6 +3,7 @@
 // end-to-end entry point.  No torch types anywhere; plain pointers and sizes.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <cuda.h>
@@ -188,6 +189,17 @@ size_t tmap_slot(const TmapKey &k) {
     return size_t(h >> 58) % kTmapCache;
 }
 }  // namespace
+
+int pdl_attr(cudaLaunchAttribute *attrs, int n) {
+    static const bool on = [] {
+        const char *e = getenv("LPY_PDL");
+        return !(e && e[0] == '0');
+    }();
+    if (!on) return n;
+    attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[n].val.programmaticStreamSerializationAllowed = 1;
+    return n + 1;
+}
 
 cudaError_t make_tmap_2d(CUtensorMap *tm, const float *base, uint64_t inner, uint64_t outer, uint64_t ld,
                          uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swizzle) {

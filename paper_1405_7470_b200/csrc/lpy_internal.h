@@ -39,6 +39,12 @@ inline cudaError_t ensure_smem_attr(F kern, int bytes, std::atomic<uint64_t> &do
     return e;
 }
 
+// Programmatic dependent launch for the library's kernels (every kernel
+// launched with it calls griddepcontrol.wait before its first global memory
+// access): on unless LPY_PDL=0.  Appends the attribute to attrs[n], returns
+// the new count.
+int pdl_attr(cudaLaunchAttribute *attrs, int n);
+
 struct Knobs {
     int num_ctas;         // 0 = auto
     int raster_group;     // 0 = auto

@@ -393,4 +393,12 @@ __device__ __forceinline__ void ld_cg_v8(const float *p, float *v) {
                  : "memory");
 }
 
+// Programmatic dependent launch: wait until the grid this one depends on in
+// stream order has completed and its memory is visible (no-op when launched
+// without the programmatic-serialization attribute or after a plain kernel),
+// and let the next grid in the stream start launching (its prologue overlaps
+// this grid's tail; it waits for this grid before touching memory itself).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 }  // namespace lpy

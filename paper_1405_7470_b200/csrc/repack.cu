@@ -5,6 +5,7 @@
 // 4 floats -- the paper's "padding" data-layout transformation
 // applied on the fly.  Bytes only: no arithmetic of the method happens here.
 #include "lpy_internal.h"
+#include "ptx.cuh"
 
 namespace lpy {
 
@@ -16,6 +17,7 @@ namespace lpy {
 // reads them: the descriptors carry the logical extent).
 constexpr int REPACK_UNROLL = 16;
 __global__ void __launch_bounds__(256) repack_kernel(RepackJob j0, RepackJob j1, int njobs) {
+    pdl_wait();                 // the operands' producer (the previous grid) is done
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     const int64_t total = j0.lines + (njobs > 1 ? j1.lines : 0);
@@ -39,6 +41,7 @@ __global__ void __launch_bounds__(256) repack_kernel(RepackJob j0, RepackJob j1,
             }
         }
     }
+    pdl_launch_dependents();
 }
 
 // Both operands' repacks (njobs = 1 or 2) in one launch.
@@ -48,8 +51,14 @@ cudaError_t launch_repack(const RepackJob *jobs, int njobs, int num_sms, cudaStr
     if (njobs <= 0 || lines <= 0) return cudaSuccess;
     int64_t blocks = (lines + 7) / 8;
     if (blocks > int64_t(num_sms) * 8) blocks = int64_t(num_sms) * 8;
-    repack_kernel<<<unsigned(blocks), 256, 0, s>>>(jobs[0], njobs > 1 ? jobs[1] : jobs[0], njobs);
-    return cudaGetLastError();
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(blocks));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_attr(attr, 0);
+    return cudaLaunchKernelEx(&cfg, repack_kernel, jobs[0], njobs > 1 ? jobs[1] : jobs[0], njobs);
 }
 
 }  // namespace lpy

@@ -34,6 +34,9 @@ CONFIGS = [
     ("2048x2048x8192", 2048, 2048, 8192, 0, 0, 0),
 ]
 paths = sys.argv[1].split(",") if len(sys.argv) > 1 else ["ffma", "3xtf32"]
+if os.environ.get("SHAPES"):   # comma-separated substrings of config names to keep
+    keep = os.environ["SHAPES"].split(",")
+    CONFIGS = [c for c in CONFIGS if any(k in c[0] for k in keep)]
 flush = torch.empty(256 * 2 ** 20 // 4, device="cuda")
 
 
