@@ -516,6 +516,41 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (ept == 0) { TL(12); TLC(3); }
                 if (ept == 0) p.sem[vt * CG + rank] = 0;   // ready for the next launch
             }
+            if (u + units >= p.num_units) {
+                // This CTA's last tile: the operand ring is idle (the final accf
+                // commit covers every MMA of the pair), so the tile goes through
+                // it and leaves row-contiguous -- a warp stores 512 consecutive
+                // bytes per instruction instead of 32 bytes of 32 rows, which
+                // halves the exposed epilogue of small products.
+                float *dst = reinterpret_cast<float *>(stages) + (quad * 32 + lane) * (BN + 4) + half * EC;
+#pragma unroll
+                for (int j = 0; j < EC; j += 4)
+                    *reinterpret_cast<float4 *>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                named_bar_sync(1, EPI_WARPS * 32);
+                int tm, tn;
+                tile_coords(t, p, tm, tn);
+                const int row0 = tm * (BM * CG) + rank * BM, colt = tn * BN;
+                constexpr int C4 = BN / 4;
+                const float *stg = reinterpret_cast<const float *>(stages);
+#pragma unroll 4
+                for (int idx = ept; idx < BM * C4; idx += EPI_WARPS * 32) {
+                    const int rl = idx / C4, c4 = idx % C4;
+                    const float4 v = *reinterpret_cast<const float4 *>(stg + rl * (BN + 4) + c4 * 4);
+                    const int row = row0 + rl, col = colt + c4 * 4;
+                    if (row < p.M) {
+                        float *c = p.C + int64_t(row) * p.ldc + col;
+                        if (p.c_vec && col + 3 < p.N) {
+                            *reinterpret_cast<float4 *>(c) = v;
+                        } else {
+                            const float o[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                if (col + e < p.N) c[e] = o[e];
+                        }
+                    }
+                }
+                continue;
+            }
             const int row = row_of(), col0 = col0_of();
             float *crow = p.C + int64_t(row) * p.ldc;
             if (row < p.M) {
