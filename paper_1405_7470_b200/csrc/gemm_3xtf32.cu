@@ -221,6 +221,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (threadIdx.x == 0) {
         TL(0);
         TLC(0);
+        // descriptor fetch overlaps the barrier / TMEM setup (kernel parameters:
+        // not written by the previous grid, so no need to wait for it)
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&ready[s], CG * XFORM_WARPS);
@@ -251,8 +255,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (warp == 0) {
             // ------------------------------------------------ TMA producer
             if (lane == 0) {
-                tma_prefetch_desc(&tmA);
-                tma_prefetch_desc(&tmB);
                 // 1: A last / B first; 2: the reverse; 3: A last / B normal;
                 // 4: B last / A normal; 5: half of A's lines evict_last
                 const uint64_t pol_a = p.l2hint == 1 || p.l2hint == 3 ? l2_policy_evict_last()
