@@ -398,3 +398,47 @@ def test_skinny_and_long_k_shapes(path, M, N, K):
     C, pad_ok = run_gemm(A, B, path=path)
     assert pad_ok
     check(C, A, B)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("n", [128, 1024, 2048])
+def test_dependent_chain_same_stream(path, n):
+    """Back-to-back products where each consumes the previous one's output on
+    the same stream: C1 = A.B, C2 = C1.B, C3 = C2^T(stored packed, ld = n+1,
+    so the repack kernel runs between).B.  With programmatic dependent launch
+    each kernel starts while its predecessor is finishing, so this checks that
+    every kernel waits (griddepcontrol.wait) before reading its operands or
+    writing C: each link must equal the same product computed in isolation,
+    bitwise, eager and inside a CUDA graph."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n)
+    A = (torch.rand(n, n, device="cuda", generator=g) * 2 - 1) / n ** 0.5
+    B = (torch.rand(n, n, device="cuda", generator=g) * 2 - 1) / n ** 0.5
+    pad = torch.zeros(n, n + 1, device="cuda")
+
+    def chain():
+        C1 = lpy.gemm(A, B, path=path)
+        C2 = lpy.gemm(C1, B, path=path)
+        pad[:, :n] = C2          # (a torch kernel between ours)
+        C3 = lpy.gemm(pad[:, :n].t(), B, path=path)   # column-major view, ld = n+1: repack
+        return C1, C2, C3
+
+    C1, C2, C3 = chain()
+    torch.cuda.synchronize()
+    # the same products one at a time, fully synchronised
+    R1 = lpy.gemm(A, B, path=path); torch.cuda.synchronize()
+    R2 = lpy.gemm(R1.clone(), B, path=path); torch.cuda.synchronize()
+    R3 = lpy.gemm(R2.t().contiguous(), B, path=path); torch.cuda.synchronize()
+    assert torch.equal(C1, R1) and torch.equal(C2, R2) and torch.equal(C3, R3)
+    # and replayed from a graph
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            G1, G2, G3 = chain()
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(3):
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(G1, R1) and torch.equal(G2, R2) and torch.equal(G3, R3)
