@@ -636,7 +636,11 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            # the arithmetic the path computes in: three tf32 tensor-core products per
+            # fp32 product, fp32 accumulation (fp32-accurate: <= 1e-5 normalised error
+            # vs the float64 oracle), or plain fp32 FMAs on the SIMT path
+            "dtype": "tf32x3+f32acc" if res["path"] == "3xtf32" else "f32",
             "data": "synthetic: seeded SplitMix64 uniform[-1,1) fp32 on a 2^-23 grid",
             "config": {"workload": f"n={n} square fp32 C=A*B, row-major A/B/C (BASELINE config 4)",
                        "path": res["path"], "M": n, "N": n, "K": n,
