@@ -612,6 +612,8 @@ def main():
     if rank == 0:
         n = args.n
         flops = 2.0 * n ** 3
+        if dist_on and args.emulate_ranks and world == 1:
+            flops /= args.emulate_ranks      # diagnostics: rank 0's panel of an N-rank split only
         ms = res["total_ms"] / args.steps
         value = flops / (ms * 1e-3) / 1e9
 

@@ -776,9 +776,14 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, const ClusterCap
     int units = (kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms) / CG;  // CTAs (pairs) in the grid
     if (units > prm.num_units) units = prm.num_units;
     if (units < 1) units = 1;
-    // cluster split: one cluster per tile, every pair runs exactly one unit
-    // (opts.num_ctas cannot shrink this grid; results do not depend on it)
-    if (prm.cluster_split) units = prm.num_units;
+    // cluster split: one cluster per tile, every pair runs exactly one unit.
+    // A grid capped by opts.num_ctas below that (dist.py's concurrent block
+    // products share the GPU) runs the same k-slices through the global-memory
+    // fix-up instead -- the same slice-order sums, so the same bits.
+    if (prm.cluster_split) {
+        if (kn.num_ctas > 0 && kn.num_ctas / CG < prm.num_units) prm.cluster_split = 0;
+        else units = prm.num_units;
+    }
     const int grid = units * CG;
     if (prm.splits > 1 && !prm.cluster_split) {
         const int split_tiles = prm.num_tiles - prm.full_tiles;

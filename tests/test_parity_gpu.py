@@ -442,3 +442,20 @@ def test_dependent_chain_same_stream(path, n):
         graph.replay()
         torch.cuda.synchronize()
         assert torch.equal(G1, R1) and torch.equal(G2, R2) and torch.equal(G3, R3)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("n", [128, 512, 1024])
+def test_cluster_split_grid_invariance(path, n):
+    """Single under-filled waves run their k-slices in thread-block clusters
+    summed through DSMEM; a grid capped by opts.num_ctas (dist.py's concurrent
+    block products) runs the same slices through global memory.  Both sum in
+    slice order, so every grid gives the same bits, within the bound."""
+    A, B = inputs(n, n, n, seed=n + 7)
+    ref, _ = run_gemm(A, B, path=path)
+    check(ref, A, B)
+    for ctas in (2, 8, 40, 148):
+        o = lpy.GemmOpts()
+        o.num_ctas = ctas
+        C, _ = run_gemm(A, B, path=path, opts=o)
+        assert np.array_equal(C, ref), ctas
