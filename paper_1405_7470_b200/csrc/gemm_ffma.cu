@@ -84,6 +84,7 @@ struct Params {
     // cluster compute the slices of one tile and sum them through distributed
     // shared memory (no ws, no fix-up kernel)
     int cluster_split;
+    int ws_stride;   // float4 stride between a thread's partial float4s: 256 (interleaved) or 1 (LPY_FFMA_PARTIAL=contig, A/B)
 };
 
 __device__ __forceinline__ void unit_range(int u, const Params &p, int &t, int &kb0, int &kb1) {
@@ -361,8 +362,11 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
             // values, contiguous) and the fix-up kernel (splitk_fixup) adds the
             // slices of each tile in slice order -- a fixed order, independent of
             // which slice finished first.
-            constexpr int PER = 8 * JN / 2;   // float4 per thread
-            float4 *mine = reinterpret_cast<float4 *>(p.ws + int64_t(u) * (BM * BN)) + threadIdx.x * PER;
+            // thread-interleaved: float4 v of thread t at [v][t], so a warp's store
+            // covers 512 contiguous bytes (a per-thread-contiguous layout put
+            // its 32 lanes 512 B apart: 32 sectors per instruction)
+            float4 *mine = reinterpret_cast<float4 *>(p.ws + int64_t(u) * (BM * BN)) +
+                           threadIdx.x * (p.ws_stride == 1 ? 8 * JN / 2 : 1);
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -370,7 +374,7 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
                     float lo0, hi0, lo1, hi1;
                     unpack2(acc2[i][jp], lo0, hi0);
                     unpack2(acc2[i][jp + 1], lo1, hi1);
-                    mine[(i * JN + jp) / 2] = make_float4(lo0, hi0, lo1, hi1);
+                    mine[((i * JN + jp) / 2) * p.ws_stride] = make_float4(lo0, hi0, lo1, hi1);
                 }
             continue;
         }
@@ -411,7 +415,7 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
 constexpr int FIXUP_PARTS = 4;
 template <int BN>
 __global__ void __launch_bounds__(CWARPS * 32) splitk_fixup_kernel(const Params p) {
-    constexpr int JN = BN / 32, PER = 8 * JN / 2;
+    constexpr int JN = BN / 32;
     constexpr int IPART = 8 / FIXUP_PARTS;
     const int t = blockIdx.x;
     const int i0 = blockIdx.y * IPART;
@@ -420,7 +424,7 @@ __global__ void __launch_bounds__(CWARPS * 32) splitk_fixup_kernel(const Params 
     int tm, tn;
     tile_coords(t, p, tm, tn);
     const float4 *base = reinterpret_cast<const float4 *>(p.ws + int64_t(t) * p.splits * (BM * BN)) +
-                         threadIdx.x * PER;
+                         threadIdx.x * (p.ws_stride == 1 ? 8 * JN / 2 : 1);   // [v][thread] within each slice's tile
     const int m0 = tm * BM, n0 = tn * BN;
 #pragma unroll
     for (int ii = 0; ii < IPART; ++ii) {
@@ -429,11 +433,11 @@ __global__ void __launch_bounds__(CWARPS * 32) splitk_fixup_kernel(const Params 
         float acc[2 * JN];
 #pragma unroll
         for (int h = 0; h < JN / 2; ++h) {
-            float4 s0 = base[i * (JN / 2) + h];
+            float4 s0 = base[(i * (JN / 2) + h) * p.ws_stride];
 #pragma unroll
             for (int sl = 1; sl < MAX_SPLITS; ++sl) {   // unrolled: every slice's load in flight
                 if (sl < p.splits) {
-                    const float4 q = base[int64_t(sl) * (BM * BN / 4) + i * (JN / 2) + h];
+                    const float4 q = base[int64_t(sl) * (BM * BN / 4) + (i * (JN / 2) + h) * p.ws_stride];
                     s0.x += q.x; s0.y += q.y; s0.z += q.z; s0.w += q.w;
                 }
             }
@@ -489,6 +493,11 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     prm.splits = choose_splits(prm.num_tiles, prm.k_blocks, kn.num_sms, min_kb, MAX_SPLITS);
     prm.num_units = prm.num_tiles * prm.splits;
     prm.ws = nullptr;
+    static const int ws_stride = [] {
+        const char *v = getenv("LPY_FFMA_PARTIAL");
+        return (v && v[0] == 'c') ? 1 : CWARPS * 32;
+    }();
+    prm.ws_stride = ws_stride;
     int grid = kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms;
     if (grid > prm.num_units) grid = prm.num_units;
     if (grid < 1) grid = 1;
