@@ -47,6 +47,20 @@
  *
  * DEGENERATE SIZES.  M == 0 or N == 0: empty domain, no-op returning LPY_OK
  * (S:295).  K == 0: C := 0, the identity of `sum`.
+ *
+ * DETERMINISM.  For a given shape, path, operand values and device (its SM
+ * count), the result is bitwise reproducible and independent of the
+ * lpy_gemm_opts scheduling knobs (num_ctas, raster_group), of the layouts of A
+ * and B, and of the stream: every element's k order is fixed by the shape
+ * (split-K slices, however scheduled -- persistent tiles, global-memory
+ * fix-up, or a thread-block cluster's distributed-shared-memory reduction --
+ * are summed in slice order).
+ *
+ * CAPTURE AND CHAINING.  Calls are stream-capturable into CUDA graphs.  The
+ * 3xTF32 and repack kernels use programmatic dependent launch: they may start
+ * their prologue while the preceding kernel in the stream finishes, but wait
+ * for it (griddepcontrol.wait) before reading A/B or writing C, so stream
+ * order semantics are unchanged.
  */
 #ifndef LPY_H
 #define LPY_H
