@@ -48,10 +48,10 @@
  * DEGENERATE SIZES.  M == 0 or N == 0: empty domain, no-op returning LPY_OK
  * (S:295).  K == 0: C := 0, the identity of `sum`.
  *
- * DETERMINISM.  For a given shape, path, operand values and device (its SM
- * count), the result is bitwise reproducible and independent of the
- * lpy_gemm_opts scheduling knobs (num_ctas, raster_group), of the layouts of A
- * and B, and of the stream: every element's k order is fixed by the shape
+ * DETERMINISM.  For a given shape, path, operand values, tile width and device
+ * (its SM count), the result is bitwise reproducible and independent of the
+ * lpy_gemm_opts scheduling knobs num_ctas and raster_group, of the layouts of
+ * A and B, and of the stream: every element's k order is fixed by the shape
  * (split-K slices, however scheduled -- persistent tiles, global-memory
  * fix-up, or a thread-block cluster's distributed-shared-memory reduction --
  * are summed in slice order).
@@ -110,9 +110,10 @@ typedef struct lpy_gemm_opts {
     int32_t tile_n;          /* output-tile width: 0 = auto (from shape and device), */
                              /* else 128 or 256 (both paths) or 192 (3xTF32 only;    */
                              /* LPY_ERR_NOT_SUPPORTED on FFMA); other values are     */
-                             /* LPY_ERR_INVALID_VALUE.  Results are identical for    */
-                             /* every tile width and grid size (each element's sum   */
-                             /* order is fixed by K alone)              */
+                             /* LPY_ERR_INVALID_VALUE.  Results do not depend on the  */
+                             /* grid (num_ctas); a different tile width can change   */
+                             /* the k-split of under-filled grids and so the last    */
+                             /* bits (always within the 1e-5 bound)                  */
     int32_t reserved[4];     /* must be 0                                            */
 } lpy_gemm_opts;
 
