@@ -242,10 +242,11 @@ def test_full_size_integer_freivalds(path):
 @pytest.mark.parametrize("path", PATHS)
 def test_tail_split_and_tile_width_grid_invariance(path):
     """Shapes whose schedule changes with the grid: the 3xTF32 tail split (90
-    pair tiles = 2 waves on 74 pairs, the last 16 tiles cut into k-slices) and
-    the tile-width choice that follows opts.num_ctas.  The split is fixed by the
-    shape and the SM count, the per-element order never depends on the tile
-    width, so every grid gives the same bits; and the result meets the bound."""
+    pair tiles = 2 waves on 74 pairs, the last 16 tiles cut into k-slices).
+    The tile width and the split are fixed by the shape and the SM count (never
+    by opts.num_ctas), so every grid gives the same bits; an explicit tile
+    width (opts.tile_n) is honoured, bitwise grid-invariant too, and meets the
+    bound."""
     A, B = inputs(2560, 2304, 1024, seed=21)
     ref, _ = run_gemm(A, B, path=path)
     check(ref, A, B)
