@@ -460,3 +460,23 @@ def test_cluster_split_grid_invariance(path, n):
         o.num_ctas = ctas
         C, _ = run_gemm(A, B, path=path, opts=o)
         assert np.array_equal(C, ref), ctas
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("M,N,K,la,lb,lc", [(1000, 1000, 1000, 0, 0, 0), (777, 1025, 1500, 1, 0, 0),
+                                            (300, 700, 4100, 0, 1, 1), (129, 257, 2049, 1, 1, 0),
+                                            (512, 384, 300, 0, 0, 1)])
+def test_cluster_split_ragged_edges(path, M, N, K, la, lb, lc):
+    """Single under-filled waves with ragged tiles, k-slices that do not divide
+    the k-blocks evenly, every operand layout and a column-major C (computed as
+    C^T = B^T A^T): the cluster split's DSMEM reduction stores only the logical
+    extent (padding untouched) and meets the bound; a capped grid (global
+    fix-up, same slices) gives the same bits."""
+    A, B = inputs(M, N, K, seed=M + K)
+    C, pad_ok = run_gemm(A, B, la, lb, lc, ldc=synth.min_ld(M, N, lc) + 3, path=path)
+    assert pad_ok
+    check(C, A, B)
+    o = lpy.GemmOpts()
+    o.num_ctas = 6
+    C2, _ = run_gemm(A, B, la, lb, lc, ldc=synth.min_ld(M, N, lc) + 3, path=path, opts=o)
+    assert np.array_equal(C, C2)
