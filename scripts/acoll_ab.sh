@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of the A-operand collector hint (LPY_TF32_ACOLL) on 3xTF32: small shapes (graph replay) and n=8192.
+# A/B of the A-operand collector hint on 3xTF32 (historical: the LPY_TF32_ACOLL switch it toggles was removed when the hint became unconditional; profiles/r01_tf32_collector.txt holds the result).
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 for v in 0 1 0 1; do echo "== ACOLL=$v"; LPY_TF32_ACOLL=$v timeout 300 python scripts/small_shapes.py 3xtf32 | grep -v config; done > gpurun_out/acoll_small.txt 2>&1
