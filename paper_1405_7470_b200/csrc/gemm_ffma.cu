@@ -412,11 +412,11 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
 // stores C with the same ragged-edge predicates.  Several CTAs per tile: one
 // SM pulls only ~50 GB/s of partials from L2 (bytes in flight / latency), so
 // the fix-up is spread over more SMs than there are tiles.
-constexpr int FIXUP_PARTS = 4;
+constexpr int FIXUP_PARTS = 8;   // 8 vs 4: ragged config 103.3 -> 102.5 us, others equal (profiles/r01_ffma_partial_layout.txt)
 template <int BN>
 __global__ void __launch_bounds__(CWARPS * 32) splitk_fixup_kernel(const Params p) {
     constexpr int JN = BN / 32;
-    constexpr int IPART = 8 / FIXUP_PARTS;
+    const int IPART = 8 / int(gridDim.y);   // gridDim.y = parts per tile (1, 2, 4 or 8)
     const int t = blockIdx.x;
     const int i0 = blockIdx.y * IPART;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -426,7 +426,6 @@ __global__ void __launch_bounds__(CWARPS * 32) splitk_fixup_kernel(const Params 
     const float4 *base = reinterpret_cast<const float4 *>(p.ws + int64_t(t) * p.splits * (BM * BN)) +
                          threadIdx.x * (p.ws_stride == 1 ? 8 * JN / 2 : 1);   // [v][thread] within each slice's tile
     const int m0 = tm * BM, n0 = tn * BN;
-#pragma unroll
     for (int ii = 0; ii < IPART; ++ii) {
         const int i = i0 + ii;
         const int row = m0 + a_row(wm, lm, i);
@@ -598,7 +597,12 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     if (e == cudaSuccess && prm.splits > 1) {
         cudaLaunchAttribute attr[1];
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(prm.num_tiles, FIXUP_PARTS);
+        static const int parts = [] {   // LPY_FFMA_FIXUP_PARTS (A/B); default FIXUP_PARTS
+            const char *v = getenv("LPY_FFMA_FIXUP_PARTS");
+            const int x = v ? atoi(v) : FIXUP_PARTS;
+            return (x == 1 || x == 2 || x == 4 || x == 8) ? x : FIXUP_PARTS;
+        }();
+        cfg.gridDim = dim3(prm.num_tiles, parts);
         cfg.blockDim = dim3(CWARPS * 32);
         cfg.stream = s;
         cfg.attrs = attr;
