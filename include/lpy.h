@@ -17,8 +17,11 @@
  * The order of the k summation is unspecified (unordered semantics,
  * P:395-401); results are accurate to
  *     max_ij |C_ij - Cexact_ij| / sum_k |A_ik||B_kj|  <=  1e-5
- * on either path, and exact when every input and partial sum is an integer
- * representable in fp32 and tf32 (readings A1, A2).
+ * on either path for FINITE inputs (with promote_kblocks <= 16, the largest
+ * value lpy_gemm_f32_ex accepts), and exact when every input and partial sum
+ * is an integer representable in fp32 and tf32 (readings A1, A2).
+ * Non-finite inputs: the FFMA path propagates Inf/NaN as IEEE fp32 FMAs do;
+ * the 3xTF32 path turns Inf into NaN (see LPY_PATH_3XTF32).
  *
  * LAYOUT.  Every operand carries a stride tag (P:278-280, P:313-315,
  * P:594-601, sections 2.1 and 2.4.3):
@@ -80,16 +83,26 @@ typedef enum { LPY_ROW_MAJOR = 0, LPY_COL_MAJOR = 1 } lpy_layout;
  *                    memory ("add_prefetch"), mbarrier producer /
  *                    consumer ring, per-thread register micro-tile ("ilp" +
  *                    "unr").  Each product and sum is an fp32 RN op.
- *  LPY_PATH_3XTF32 : tcgen05 tensor cores, kind::tf32, with each fp32 operand
- *                    split x = hi + lo (hi = rna_tf32(x), lo = rna_tf32(x-hi))
- *                    and C += A_lo B_hi + A_hi B_lo + A_hi B_hi accumulated in
- *                    TMEM and promoted to fp32 registers periodically.
+ *  LPY_PATH_3XTF32 : tcgen05 tensor cores, kind::tf32.  The tensor core reads
+ *                    an fp32 operand as tf32 by TRUNCATING its 13 low mantissa
+ *                    bits (measured, reading A9), so each fp32 x is
+ *                    used as big = x (seen as trunc_tf32(x)) plus
+ *                    small = rna_tf32(x - trunc_tf32(x)), and
+ *                    C += A_big B_small + A_big B_big + A_small B_big
+ *                    (small*small dropped; issued in that order) accumulated in
+ *                    TMEM, which rounds toward zero, and promoted into fp32
+ *                    registers (round-to-nearest) every promote_kblocks k-blocks.
+ *                    INPUTS MUST BE FINITE on this path: an Inf operand makes
+ *                    x - trunc(x) = Inf - Inf = NaN, so the result is NaN where
+ *                    the FFMA path would give Inf (reading A11).
  *  LPY_PATH_AUTO   : the library picks (lpy_select_path says which). */
 typedef enum { LPY_PATH_AUTO = 0, LPY_PATH_FFMA = 1, LPY_PATH_3XTF32 = 2 } lpy_path;
 
 typedef enum {
     LPY_OK = 0,
-    LPY_ERR_INVALID_VALUE = 1,      /* M/N/K < 0 or > INT32_MAX, bad enum value          */
+    LPY_ERR_INVALID_VALUE = 1,      /* M/N/K < 0 or > 2^31 - 1024, bad enum value, an    */
+                                    /* operand spanning >= 2^62 elements, or an opts     */
+                                    /* field out of range                                */
     LPY_ERR_INVALID_LD = 2,         /* ld below the minimum stated under LAYOUT          */
     LPY_ERR_NULL_POINTER = 3,       /* NULL operand with a nonzero footprint             */
     LPY_ERR_MISALIGNED = 4,         /* operand pointer not 4-byte aligned                */
@@ -105,8 +118,10 @@ typedef enum {
 typedef struct lpy_gemm_opts {
     int32_t num_ctas;        /* persistent grid size; 0 = one CTA (pair) per SM      */
     int32_t raster_group;    /* output-tile rows per rasterisation group; 0 = auto   */
-    int32_t promote_kblocks; /* 3xTF32: k-blocks per TMEM partial before promotion;  */
-                             /* 0 = auto                                             */
+    int32_t promote_kblocks; /* 3xTF32: k-blocks (16 of K each) per TMEM partial     */
+                             /* before promotion; 0 = auto (8); 1..16, larger values */
+                             /* are LPY_ERR_INVALID_VALUE (32 measured 1.05e-5 on    */
+                             /* uniform[0,1) at K = 8192: beyond the contract)       */
     int32_t tile_n;          /* output-tile width: 0 = auto (from shape and device), */
                              /* else 128 or 256 (both paths) or 192 (3xTF32 only;    */
                              /* LPY_ERR_NOT_SUPPORTED on FFMA); other values are     */

@@ -294,11 +294,28 @@ def saxpy_host(alpha, x, y, stream=None):
     return y
 
 
-def _points(p, name):
+def _points(p, name, device=None):
+    """Row stride (ELEMENTS) of an (n, >=3) fp32 point array with unit column
+    stride, on `device` ("cuda" / "cpu") when given."""
     import torch
-    if p.dtype != torch.float32 or p.dim() != 2 or p.shape[1] < 3 or (p.shape[0] > 1 and p.stride(1) != 1):
+    if not isinstance(p, torch.Tensor) or p.dtype != torch.float32 or p.dim() != 2 or p.shape[1] < 3 or \
+            (p.shape[0] >= 1 and p.stride(1) != 1):
         raise TypeError(f"{name} must be an (n, >=3) fp32 tensor with unit column stride")
+    if device is not None and p.device.type != device:
+        raise ValueError(f"{name} must be a {device} tensor")
+    if p.shape[0] > 1 and p.stride(0) < 3:
+        raise ValueError(f"{name}: rows overlap (row stride {p.stride(0)} < 3)")
     return p.stride(0) if p.shape[0] > 1 else max(3, p.shape[1])
+
+
+def _vector_arg(v, name, n, device):
+    """Check a contiguous (n,) fp32 tensor on `device` ("cuda" / "cpu")."""
+    import torch
+    if not isinstance(v, torch.Tensor) or v.dtype != torch.float32 or v.dim() != 1 or v.shape[0] != n or \
+            (n > 1 and v.stride(0) != 1):
+        raise TypeError(f"{name} must be a contiguous ({n},) fp32 tensor")
+    if v.device.type != device:
+        raise ValueError(f"{name} must be a {device} tensor")
 
 
 def coulomb(targets, sources, charges, out=None, stream=None):
@@ -307,13 +324,12 @@ def coulomb(targets, sources, charges, out=None, stream=None):
     targets (nt, >=3), sources (ns, >=3): x, y, z in the first three columns;
     charges (ns,) contiguous; returns phi (nt,)."""
     import torch
-    ldt, lds = _points(targets, "targets"), _points(sources, "sources")
-    if charges.dtype != torch.float32 or charges.dim() != 1 or charges.shape[0] != sources.shape[0] or \
-            (charges.shape[0] > 1 and charges.stride(0) != 1):
-        raise TypeError("charges must be a contiguous (ns,) fp32 tensor")
+    ldt, lds = _points(targets, "targets", "cuda"), _points(sources, "sources", "cuda")
+    _vector_arg(charges, "charges", sources.shape[0], "cuda")
     nt = targets.shape[0]
     if out is None:
         out = torch.empty(nt, dtype=torch.float32, device=targets.device)
+    _vector_arg(out, "out", nt, "cuda")
     st = _on_device((targets, sources, charges, out), stream, lambda sh: lpy_coulomb_f32(
         nt, targets.data_ptr(), ldt, sources.shape[0], sources.data_ptr(), lds, charges.data_ptr(),
         out.data_ptr(), sh))
@@ -324,7 +340,9 @@ def coulomb(targets, sources, charges, out=None, stream=None):
 
 def coulomb_host(targets, sources, charges, out, stream=None):
     """End-to-end Coulomb on host (CPU, ideally pinned) tensors; synchronises."""
-    ldt, lds = _points(targets, "targets"), _points(sources, "sources")
+    ldt, lds = _points(targets, "targets", "cpu"), _points(sources, "sources", "cpu")
+    _vector_arg(charges, "charges", sources.shape[0], "cpu")
+    _vector_arg(out, "out", targets.shape[0], "cpu")
     st = lpy_coulomb_f32_host(targets.shape[0], targets.data_ptr(), ldt, sources.shape[0], sources.data_ptr(),
                               lds, charges.data_ptr(), out.data_ptr(),
                               _stream_handle(stream) if stream is not None else None)

@@ -22,8 +22,12 @@ lpy_status cuda_fail(cudaError_t e) {
     return LPY_ERR_CUDA;
 }
 
-constexpr int64_t kMaxDim = INT32_MAX;
+// M, N, K <= 2^31 - 1024: the kernels round dimensions up to whole tiles and
+// k-blocks in 32-bit int arithmetic, which must not overflow (include/lpy.h).
+constexpr int64_t kMaxDim = INT32_MAX - 1023;
 constexpr int64_t kMaxLd = (int64_t(1) << 40) / 4 - 1;  // TMA: global strides < 2^40 bytes
+constexpr int64_t kMaxFootprint = int64_t(1) << 62;      // elements an operand may span
+constexpr int kMaxPromote = 16;                          // 3xTF32 partial length bound (1e-5 contract)
 
 struct Operand {
     const float *p;
@@ -40,6 +44,10 @@ bool valid_layout(int l) { return l == LPY_ROW_MAJOR || l == LPY_COL_MAJOR; }
 lpy_status validate_operand(const Operand &o) {
     const int64_t need = o.inner() > 1 ? o.inner() : 1;
     if (o.ld < need || o.ld > kMaxLd) return LPY_ERR_INVALID_LD;
+    // (lines-1)*ld + inner must stay far from int64 overflow before extent()
+    // multiplies it out (lines <= 2^31, ld < 2^38, so the product can pass 2^63)
+    if (o.rows > 0 && o.cols > 0 && o.lines() - 1 > (kMaxFootprint - o.inner()) / o.ld)
+        return LPY_ERR_INVALID_VALUE;
     if (o.extent() > 0) {
         if (o.p == nullptr) return LPY_ERR_NULL_POINTER;
         if (reinterpret_cast<uintptr_t>(o.p) & 3) return LPY_ERR_MISALIGNED;
@@ -63,7 +71,8 @@ lpy_status validate_all(int64_t M, int64_t N, int64_t K, const Operand &A, const
     if (path != LPY_PATH_AUTO && path != LPY_PATH_FFMA && path != LPY_PATH_3XTF32)
         return LPY_ERR_INVALID_VALUE;
     if (opts) {
-        if (opts->num_ctas < 0 || opts->raster_group < 0 || opts->promote_kblocks < 0)
+        if (opts->num_ctas < 0 || opts->raster_group < 0 || opts->promote_kblocks < 0 ||
+            opts->promote_kblocks > kMaxPromote)
             return LPY_ERR_INVALID_VALUE;
         if (opts->tile_n != 0 && opts->tile_n != 128 && opts->tile_n != 192 && opts->tile_n != 256)
             return LPY_ERR_INVALID_VALUE;

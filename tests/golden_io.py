@@ -61,13 +61,16 @@ def coulomb_golden_files():
 
 
 def read_coulomb_golden(name):
-    """(sources (ns,3) f32, charges (ns,) f32, targets (nt,3) f32, expected phi (nt,))."""
+    """(sources (ns,3) f32, charges (ns,) f32, targets (nt,3) f32, expected phi (nt,),
+    expected normaliser D (nt,) = sum_j |q_j| / r_ij, worked by hand in each file)."""
     lines = [ln.split("#", 1)[0].strip() for ln in open(os.path.join(COULOMB_DIR, name))]
     lines = [ln for ln in lines if ln]
     i_t, i_p = lines.index("targets x y z"), lines.index("phi")
+    i_d = lines.index("D")
     assert lines[0] == "sources x y z q"
     src = np.array([[float(v) for v in ln.split()] for ln in lines[1:i_t]])
     tgt = np.array([[float(v) for v in ln.split()] for ln in lines[i_t + 1:i_p]])
-    phi = np.array([float(ln) for ln in lines[i_p + 1:]])
-    assert src.shape[1] == 4 and tgt.shape[1] == 3 and phi.shape[0] == tgt.shape[0]
-    return (src[:, :3].astype(np.float32), src[:, 3].astype(np.float32), tgt.astype(np.float32), phi)
+    phi = np.array([float(ln) for ln in lines[i_p + 1:i_d]])
+    D = np.array([float(ln) for ln in lines[i_d + 1:]])
+    assert src.shape[1] == 4 and tgt.shape[1] == 3 and phi.shape[0] == tgt.shape[0] == D.shape[0]
+    return (src[:, :3].astype(np.float32), src[:, 3].astype(np.float32), tgt.astype(np.float32), phi, D)

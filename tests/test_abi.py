@@ -66,7 +66,10 @@ def call(M=4, N=4, K=4, A=FAKE, lda=4, la=0, B=FAKE + (1 << 20), ldb=4, lb=0,
 
 
 @pytest.mark.parametrize("kw,code", [
-    (dict(M=-1), 1), (dict(K=-3), 1), (dict(N=1 << 31), 1),
+    (dict(M=-1), 1), (dict(K=-3), 1), (dict(N=1 << 31), 1), (dict(K=(1 << 31) - 1023), 1),
+    (dict(N=(1 << 31) - 1023, ldb=(1 << 31) - 1023, ldc=(1 << 31) - 1023), 1),
+    # a footprint past 2^62 elements: (lines-1)*ld would overflow int64
+    (dict(M=(1 << 31) - 1024, lda=(1 << 38) - 1, K=4), 1),
     (dict(la=2), 1), (dict(lc=-1), 1), (dict(path=3), 1),
     (dict(lda=3), 2), (dict(ldb=0), 2), (dict(ldc=3), 2), (dict(la=1, lda=3), 2),
     (dict(M=5, la=1, lda=4), 2), (dict(lda=1 << 40), 2),
@@ -88,6 +91,14 @@ def test_bad_opts_rejected():
     o = lpy.GemmOpts()
     o.num_ctas = -2
     assert call(opts=o) == 1
+    # promotion intervals beyond 16 k-blocks break the 1e-5 contract (lpy.h)
+    o = lpy.GemmOpts()
+    o.promote_kblocks = 17
+    assert call(opts=o) == 1
+    o.promote_kblocks = 16                 # accepted: fails later, in the device query
+    import torch
+    if not torch.cuda.is_available():
+        assert call(opts=o) in (6, 8)
 
 
 def test_empty_domain_is_noop_without_cuda():
@@ -167,3 +178,26 @@ def test_coulomb_validation_errors_precede_cuda(kw, code, host):
 @pytest.mark.parametrize("host", [False, True])
 def test_coulomb_empty_targets_is_a_noop(host):
     assert coulomb_call(nt=0, t=0, phi=0, host=host) == 0
+
+
+def test_coulomb_binding_checks_arguments_before_the_library():
+    """out / charges / point arrays are checked in the binding (a short,
+    strided or float64 `out` would otherwise be overrun or silently garbage)."""
+    import torch
+    P = torch.zeros(4, 3)
+    q = torch.zeros(4)
+    # a (1, 3) view whose column stride is not 1 (X.T[:1] of a (3, n) tensor)
+    with pytest.raises(TypeError, match="unit column stride"):
+        lpy.coulomb_host(torch.zeros(3, 5).T[:1], P, q, torch.zeros(1))
+    with pytest.raises(TypeError, match="out"):
+        lpy.coulomb_host(P, P, q, torch.zeros(3))                       # short out
+    with pytest.raises(TypeError, match="out"):
+        lpy.coulomb_host(P, P, q, torch.zeros(4, dtype=torch.float64))  # wrong dtype
+    with pytest.raises(TypeError, match="out"):
+        lpy.coulomb_host(P, P, q, torch.zeros(8)[::2])                  # strided
+    with pytest.raises(TypeError, match="charges"):
+        lpy.coulomb_host(P, P, torch.zeros(3), torch.zeros(4))          # short charges
+    with pytest.raises(ValueError, match="cuda"):
+        lpy.coulomb(P, P, q)                                            # host tensors to the device entry
+    with pytest.raises(ValueError, match="overlap"):
+        lpy.coulomb_host(torch.zeros(12).as_strided((4, 3), (2, 1)), P, q, torch.zeros(4))
