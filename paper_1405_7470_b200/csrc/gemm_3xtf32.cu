@@ -44,7 +44,8 @@
 namespace lpy {
 namespace tf32 {
 
-constexpr int MAX_SPLITS = 4;                // k-slices per split tile (tail_split caps S)
+constexpr int MAX_SPLITS = 4;                // k-slices per split tile (cluster split)
+constexpr int MAX_PIECES = 5;                // pieces of a split tile: stream-K <= SK_MAX_PIECES + 1
 constexpr int BM = 128, BK = 16;             // BM rows per CTA (the tile's BN columns: template, 128/192/256)
 constexpr int THREADS = 512;                 // 16 warps = 4 warpgroups
 constexpr int XFORM_WARP0 = 4, XFORM_WARPS = 4;
@@ -71,34 +72,103 @@ struct Params {
     int64_t ldc;
     int tiles_m, tiles_n, num_tiles, k_blocks, group, promote;
     int c_vec;          // C rows 16-byte aligned (float4 stores)
-    int l2hint;         // 0: no L2 hints; 1-5: eviction-priority experiments (LPY_L2HINT)
     int c_vec8;         // C rows 32-byte aligned (STG.256)
     long long *trace;   // diagnostics build only (-DLPY_TRACE): per-CTA cycle counters
-    // Tail split (the ragged last wave): tiles [0, full_tiles) are one work unit
-    // each; every later tile is split into `splits` k-slices, so the last wave
-    // of short units fills all CTA pairs.  Slice partials are parked in `ws` and
-    // the slice that finishes a tile last adds them in slice order.
+    // Work units.  Tiles [0, full_tiles) are one unit each.  The later tiles
+    // (the ragged last wave) are cut along k in one of two ways:
+    //  * stream-K (sk_workers > 0; >= 2 waves): the tail's sk_iters =
+    //    (num_tiles - full_tiles) * k_blocks k-block iterations are dealt out
+    //    evenly to sk_workers "workers" -- worker w takes iterations
+    //    [floor(w*W/P'), floor((w+1)*W/P')) of the tail tiles in order -- so the
+    //    last wave is (tail tiles / P') of a tile long for every CTA pair, a
+    //    fractional split.  A worker's range is at most one tile
+    //    long, so it covers at most two pieces (the end of one tile, the start
+    //    of the next): unit full_tiles + piece * sk_stride + w, empty when
+    //    w >= sk_workers or the range does not reach a second tile.  With the
+    //    whole grid of sk_stride pairs, pair w runs worker w's pieces.
+    //  * equal slices (splits > 1, sk_workers == 0): every tail tile is cut into
+    //    `splits` k-slices, unit full_tiles + tail_tile * splits + slice (the
+    //    cluster split's global-memory fallback for a capped grid).
+    // A tile cut into several pieces has each piece park its partial in `ws`
+    // (slot = the unit's index past full_tiles); the piece that finishes last
+    // adds them in k order -- a fixed order, so results are deterministic and
+    // independent of the grid.
     int full_tiles, splits, num_units;
+    int sk_workers, sk_stride;
+    long long sk_iters;
     // cluster split (a single under-filled wave): every tile is cut into
     // `splits` k-slices computed by the `splits` CTA pairs of one cluster, whose
     // partials are summed through distributed shared memory (no ws / sem)
     int cluster_split;
     float *ws;          // [(num_units - full_tiles)][CG][BM x BN] partial tiles
-    int *sem;           // [(num_tiles - full_tiles)][CG] arrival counters, zero on entry and exit
+    int *sem;           // 2 x [(num_tiles - full_tiles)][CG] ticket / written counters, zero on entry and exit
 };
 
-// Work unit u -> tile t, k-block range [kb0, kb1), and (for a split unit) its
-// index among the split units (-1 for a whole tile).
+// Stream-K: the worker whose iteration range contains tail iteration x
+// (b(w) = floor(w W / P') <= x < b(w+1)), and b(w) itself.
+__device__ __forceinline__ int sk_worker_of(long long x, const Params &p) {
+    return int(((x + 1) * p.sk_workers + p.sk_iters - 1) / p.sk_iters) - 1;
+}
+__device__ __forceinline__ long long sk_begin(int w, const Params &p) {
+    return (static_cast<long long>(w) * p.sk_iters) / p.sk_workers;
+}
+
+// Work unit u -> tile t, k-block range [kb0, kb1) (empty when kb0 >= kb1), and
+// for a piece of a tile cut into several its partial slot (-1 for a tile done
+// by one unit).
 __device__ __forceinline__ void unit_range(int u, const Params &p, int &t, int &kb0, int &kb1, int &su) {
     if (u < p.full_tiles) {
         t = u; kb0 = 0; kb1 = p.k_blocks; su = -1;
         return;
     }
     su = u - p.full_tiles;
+    if (p.sk_workers > 0) {
+        // (running the pieces FIRST, so that their fix-ups overlap later whole
+        // tiles, measured slower: the fix-up then stalls its pair's next tile,
+        // profiles/r02_streamk.txt)
+        const int piece = su / p.sk_stride, w = su - piece * p.sk_stride;
+        t = p.full_tiles; kb0 = kb1 = 0;
+        if (w >= p.sk_workers) return;
+        const long long b0 = sk_begin(w, p), b1 = sk_begin(w + 1, p), kb = p.k_blocks;
+        const long long vt = b0 / kb + piece;                  // tail tile of this piece
+        const long long lo = max(b0, vt * kb), hi = min(b1, (vt + 1) * kb);
+        if (lo >= hi) return;
+        t = p.full_tiles + int(vt);
+        kb0 = int(lo - vt * kb);
+        kb1 = int(hi - vt * kb);
+        // a piece covering its whole tile is the tile's only unit
+        if (kb0 == 0 && kb1 == p.k_blocks) su = -1;
+        return;
+    }
     const int v = su / p.splits, sl = su - v * p.splits;
     t = p.full_tiles + v;
     kb0 = int((int64_t(sl) * p.k_blocks) / p.splits);
     kb1 = int((int64_t(sl + 1) * p.k_blocks) / p.splits);
+}
+
+// The pieces of split tail tile vt in k order: count, and the partial slot of
+// the i-th.
+__device__ __forceinline__ int split_pieces(int vt, const Params &p) {
+    if (p.sk_workers == 0) return p.splits;
+    const long long kb = p.k_blocks;
+    return sk_worker_of((vt + 1) * kb - 1, p) - sk_worker_of(vt * kb, p) + 1;
+}
+__device__ __forceinline__ int split_slot(int vt, int i, const Params &p) {
+    if (p.sk_workers == 0) return vt * p.splits + i;
+    const long long kb = p.k_blocks;
+    const int w = sk_worker_of(vt * kb, p) + i;
+    const int piece = int(sk_begin(w, p) / kb) == vt ? 0 : 1;
+    return piece * p.sk_stride + w;
+}
+
+// Whether any unit after u (stride `units`) of this pair is non-empty.
+__device__ __forceinline__ bool more_work_after(int u, int units, const Params &p) {
+    for (int v = u + units; v < p.num_units; v += units) {
+        int t, kb0, kb1, su;
+        unit_range(v, p, t, kb0, kb1, su);
+        if (kb0 < kb1) return true;
+    }
+    return false;
 }
 
 // Cycle accounting for the diagnostics build (liblpy_trace.so); compiled out of
@@ -117,13 +187,16 @@ __device__ __forceinline__ void unit_range(int u, const Params &p, int &t, int &
             p.trace[gridDim.x * 8 + (slot)] = (long long)g_;                          \
         }                                                                             \
     } while (0)
-// every CTA's entry / exit time, after the timeline
+// every CTA's event times (12 slots: 0 entry, 1 exit, 2 fix-up start, 3 fix-up
+// loads done, 4 MMA loop done, 5 last partial promoted, 6 first split unit's
+// first MMA, 7 fix-up: other pieces written, 8 / 9 a writer's ticket / partial
+// written), after the timeline
 #define TLC(which)                                                                    \
     do {                                                                              \
         if (p.trace) {                                                                \
             unsigned long long g_;                                                    \
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                    \
-            p.trace[gridDim.x * 8 + 16 + 4 * blockIdx.x + (which)] = (long long)g_;   \
+            p.trace[gridDim.x * 8 + 16 + 12 * blockIdx.x + (which)] = (long long)g_;   \
         }                                                                             \
     } while (0)
 #else
@@ -255,19 +328,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (warp == 0) {
             // ------------------------------------------------ TMA producer
             if (lane == 0) {
-                // 1: A last / B first; 2: the reverse; 3: A last / B normal;
-                // 4: B last / A normal; 5: half of A's lines evict_last
-                const uint64_t pol_a = p.l2hint == 1 || p.l2hint == 3 ? l2_policy_evict_last()
-                                       : p.l2hint == 2               ? l2_policy_evict_first()
-                                       : p.l2hint == 5               ? l2_policy_evict_last_frac(0.5f)
-                                                                     : l2_policy_evict_normal();
-                const uint64_t pol_b = p.l2hint == 1 ? l2_policy_evict_first()
-                                       : p.l2hint == 2 || p.l2hint == 4 ? l2_policy_evict_last()
-                                                                        : l2_policy_evict_normal();
-                auto load = [&](void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1, uint64_t pol) {
-                    if (p.l2hint) tma_load_2d_hint(dst, tm, bar, c0, c1, pol);
-                    else          tma_load_2d(dst, tm, bar, c0, c1);
-                };
                 int s = 0;
                 uint32_t ph = 0;
                 for (int u = unit0; u < p.num_units; u += units) {
@@ -287,16 +347,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                         if constexpr (AMN) {
 #pragma unroll
                             for (int j = 0; j < BM / 32; ++j)
-                                load(sa + j * 2048, &tmA, &full[s], m0 + 32 * j, k0, pol_a);
+                                tma_load_2d(sa + j * 2048, &tmA, &full[s], m0 + 32 * j, k0);
                         } else {
-                            load(sa, &tmA, &full[s], k0, m0, pol_a);
+                            tma_load_2d(sa, &tmA, &full[s], k0, m0);
                         }
                         if constexpr (BMN) {
 #pragma unroll
                             for (int j = 0; j < C_::BN_CTA / 32; ++j)
-                                load(sb + j * 2048, &tmB, &full[s], n0 + 32 * j, k0, pol_b);
+                                tma_load_2d(sb + j * 2048, &tmB, &full[s], n0 + 32 * j, k0);
                         } else {
-                            load(sb, &tmB, &full[s], k0, n0, pol_b);
+                            tma_load_2d(sb, &tmB, &full[s], k0, n0);
                         }
                         if (kb == kb0 && u == unit0) TL(2);
                         if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -336,6 +396,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     mbar_wait(&ready[s], ph);
                     TR_ADD(1, t_r);
                     if (kb == kb0 && u == unit0 && lane == 0) TL(4);
+                    if (kb == kb0 && su >= 0 && lane == 0 && su < p.sk_stride) TLC(6);
                     tc_fence_after();
                     const uint32_t d = tmem + b * 256;
                     const uint64_t off = uint64_t(s) * STEP;
@@ -371,6 +432,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
             TR_ADD(0, t_all);
+            if (lane == 0) TLC(4);
         }
     } else if (warp < EPI_WARP0) {
         // ------------------------------------------------ split transform (WG1)
@@ -418,6 +480,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int u = unit0; u < p.num_units; u += units) {
             int t, kb0, kb1, su;
             unit_range(u, p, t, kb0, kb1, su);
+            if (kb0 >= kb1) continue;
             const int parts_per_tile = (kb1 - kb0 + p.promote - 1) / p.promote;
             float acc[EC];
 #pragma unroll
@@ -452,7 +515,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             // each instruction writes whole sectors of 32 rows
             // (computed where used: live across the partial's write they cost
             // the BN = 256 variants register spills)
-            if (ept == 0) TL(9);
+            if (ept == 0) { TL(9); TLC(5); }
             auto row_of = [&]() {
                 int tm, tn;
                 tile_coords(t, p, tm, tn);
@@ -476,49 +539,85 @@ __global__ void __launch_bounds__(THREADS, 1)
                 continue;
             }
             if (su >= 0) {
-                // split tile: park this slice's partial as thread-interleaved
-                // 32-byte vectors (a warp writes 1 KB contiguous), count arrivals
-                // per (tile, CTA); the last slice sums all partials in slice order
-                // and stores.
+                // A tile cut into pieces.  Each piece takes a ticket per (tile,
+                // CTA); all but the last park their partial as thread-
+                // interleaved 32-byte vectors (a warp writes and later reads
+                // 1 KB contiguous) and count themselves written.  The last
+                // waits for those writes -- the writers already hold tickets,
+                // so they are running and the wait is bounded (no spin on a
+                // CTA that may not be resident) -- and sums the pieces in k
+                // order with its own partial taken from registers: it neither
+                // writes nor re-reads it, and reads the others with 32-byte
+                // loads.  The order of the additions is fixed
+                // by the decomposition, never by who finishes last.
                 constexpr int TILE8 = BM * BN / 8;
-                float *mine = p.ws + ((int64_t(su) * CG + rank) * TILE8 + ept) * 8;
-#pragma unroll
-                for (int j = 0; j < EC; j += 8) st_cg_v8(mine + (j / 8) * 256 * 8, &acc[j]);
-                if (ept == 0) TL(10);
-                __threadfence();
-                named_bar_sync(1, EPI_WARPS * 32);
-                if (ept == 0) TL(11);
                 const int vt = t - p.full_tiles;
-                if (ept == 0) last_flag = (atomicAdd(p.sem + vt * CG + rank, 1) == p.splits - 1);
+                const int npieces = split_pieces(vt, p);
+                const int me = p.sk_workers > 0
+                                   ? su % p.sk_stride - sk_worker_of(static_cast<long long>(vt) * p.k_blocks, p)
+                                   : su - vt * p.splits;
+                int *arrive = p.sem + vt * CG + rank;
+                int *written = p.sem + (p.num_tiles - p.full_tiles + vt) * CG + rank;
+                if (ept == 0) last_flag = atomicAdd(arrive, 1) == npieces - 1;
                 named_bar_sync(1, EPI_WARPS * 32);
-                if (!last_flag) continue;
-                if (ept == 0) TLC(2);
-                __threadfence();
-                // sum the slices in slice order into acc (the own partial is
-                // re-read like the others), slice by slice so that all of a
-                // slice's loads are in flight at once: one SM pulls only ~50 GB/s
-                // from L2 (bytes in flight / latency), so the fix-up costs
-                // ~2.5 us per 128 KB partial
-                const float4 *base = reinterpret_cast<const float4 *>(
-                    p.ws + ((int64_t(vt) * p.splits * CG + rank) * TILE8 + ept) * 8);
-                const int64_t slice4 = int64_t(CG) * TILE8 * 2;
+                if (!last_flag) {
+                    if (ept == 0) TLC(8);
+                    float *mine = p.ws + ((int64_t(su) * CG + rank) * TILE8 + ept) * 8;
 #pragma unroll
-                for (int j = 0; j < EC; j += 4) {
-                    const float4 q = __ldcg(base + (j / 8) * 256 * 2 + (j % 8) / 4);
-                    acc[j] = q.x; acc[j + 1] = q.y; acc[j + 2] = q.z; acc[j + 3] = q.w;
+                    for (int j = 0; j < EC; j += 8) st_cg_v8(mine + (j / 8) * 256 * 8, &acc[j]);
+                    if (ept == 0) TL(10);
+                    __threadfence();
+                    named_bar_sync(1, EPI_WARPS * 32);
+                    if (ept == 0) { atomicAdd(written, 1); TLC(9); }
+                    continue;
+                }
+                if (ept == 0) {
+                    TLC(2);
+                    while (ld_acquire_gpu(written) < npieces - 1) __nanosleep(64);
+                    TLC(7);
+                    *arrive = 0;      // ready for the next launch (nobody else touches them now)
+                    *written = 0;
+                }
+                named_bar_sync(1, EPI_WARPS * 32);
+                __threadfence();
+                // Sum in k order, ((p0 + p1) + p2) + ...  With the own piece
+                // first or second, acc (= p_me) is the running sum from the
+                // start (p1 + p0 == p0 + p1 bitwise: addition commutes).  A
+                // later own piece (rare: the last to finish is usually the
+                // tile's first or second piece) is written out and the sum
+                // rebuilt from memory in order.
+                auto slot_ptr = [&](int i) {
+                    return p.ws + ((int64_t(split_slot(vt, i, p)) * CG + rank) * TILE8 + ept) * 8;
+                };
+                int i0 = 0;
+                if (me >= 2) {
+                    float *mine = slot_ptr(me);
+#pragma unroll
+                    for (int j = 0; j < EC; j += 8) st_cg_v8(mine + (j / 8) * 256 * 8, &acc[j]);
+                    const float *src = slot_ptr(0);
+#pragma unroll
+                    for (int j = 0; j < EC; j += 8) ld_cg_v8(src + (j / 8) * 256 * 8, &acc[j]);
+                    i0 = 1;
                 }
 #pragma unroll 1
-                for (int sl = 1; sl < p.splits; ++sl) {
+                for (int i = i0; i < npieces; ++i) {
+                    if (i == me && me < 2) continue;
+                    // (the own piece re-read when me >= 2 was written by this
+                    // thread: the volatile load keeps it after that store)
+                    const float *src = slot_ptr(i) + opaque_zero();
+                    const bool own = i == me;
 #pragma unroll
-                    for (int j = 0; j < EC; j += 4) {
-                        const float4 q = __ldcg(base + sl * slice4 + (j / 8) * 256 * 2 + (j % 8) / 4);
-                        acc[j] += q.x; acc[j + 1] += q.y; acc[j + 2] += q.z; acc[j + 3] += q.w;
+                    for (int j = 0; j < EC; j += 8) {
+                        float v[8];
+                        if (own) ld_cg_v8(src + (j / 8) * 256 * 8, v);
+                        else     ld_cg_v8_nv(src + (j / 8) * 256 * 8, v);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) acc[j + e] += v[e];
                     }
                 }
                 if (ept == 0) { TL(12); TLC(3); }
-                if (ept == 0) p.sem[vt * CG + rank] = 0;   // ready for the next launch
             }
-            if (u + units >= p.num_units) {
+            if (!more_work_after(u, units, p)) {
                 // This CTA's last tile: the operand ring is idle (the final accf
                 // commit covers every MMA of the pair), so the tile goes through
                 // it and leaves row-contiguous -- a warp stores 512 consecutive
@@ -651,11 +750,16 @@ static cudaError_t launch_t(const CUtensorMap &ta, const CUtensorMap &tb, const 
 
 static long long *g_trace = nullptr;   // set by lpy_trace_set_buffer (diagnostics build)
 
-// Split of the last wave into k-slices, fixed by the shape and the device
-// (never by opts.num_ctas, so results stay bitwise grid-invariant):
-//  * >= 2 waves with a partial last one: its `rem` tiles are cut into
-//    S = floor(pairs / rem) slices (<= 4, >= 16 k-blocks each), so the last
-//    wave is S times shorter;
+// Split of the last wave along k, fixed by the shape and the device (never by
+// opts.num_ctas, so results stay bitwise grid-invariant):
+//  * >= 2 waves with a partial last one: stream-K over the last wave's `rem`
+//    tiles.  Their rem * k_blocks iterations are dealt out evenly to
+//    P' = min(pairs, 4 rem, rem k_blocks / 16) workers (<= 4 pieces per tile
+//    + 1, >= 16 k-blocks per worker), so the last wave takes rem / P' of a
+//    tile instead of a whole one -- a fractional split (the paper's "separate
+//    code for edge and corner cases").  Used when it shortens the
+//    last wave by >= 20% and K >= 4096.  (Round 1 cut the tail tiles into S = floor(pairs /
+//    rem) equal slices: at 128 tiles on 74 pairs, S = 1, no gain.)
 //  * a single under-filled wave (tiles < pairs, e.g. n = 1024): every tile is
 //    cut into S = 2 or 4 k-slices (S * tiles <= pairs, >= 8 k-blocks each)
 //    computed by the S CTA pairs of one cluster (2S CTAs), which sum their
@@ -667,22 +771,35 @@ static long long *g_trace = nullptr;   // set by lpy_trace_set_buffer (diagnosti
 //    hardware co-schedules a cluster's CTAs.  LPY_TF32_SPLIT1=0 disables it.
 //    S = 4 needs clusters of 8 CTAs, of which only `caps.max8` fit on the chip
 //    at once (a cluster lives in one GPC), so S follows what fits in one wave.
+// LPY_TF32_STREAMK=0 disables the stream-K tail (diagnostics / A-B).
 struct ClusterCaps { int max4, max8; };   // co-resident clusters of 4 / 8 CTAs
-struct TailSplit { int splits, full_tiles, num_units, cluster; };
+struct TailSplit {
+    int splits, full_tiles, num_units, cluster;
+    int sk_workers, sk_stride;
+    long long sk_iters;
+    double waves;          // modelled length of the schedule in whole-tile waves
+};
+constexpr int SK_MAX_PIECES = 4;        // workers per tail tile (fix-up reads)
+constexpr int SK_MIN_KB = 16;           // k-blocks per stream-K worker
+constexpr int SK_MIN_TILE_KB = 256;     // stream-K only for K >= 4096
 static TailSplit tail_split(int num_tiles, int k_blocks, int pairs, const ClusterCaps &caps) {
     static const bool split1 = [] {
         const char *e = getenv("LPY_TF32_SPLIT1");
         return !(e && e[0] == '0');
     }();
-    TailSplit r{1, num_tiles, num_tiles, 0};
+    static const bool streamk = [] {
+        const char *e = getenv("LPY_TF32_STREAMK");
+        return !(e && e[0] == '0');
+    }();
+    TailSplit r{1, num_tiles, num_tiles, 0, 0, 0, 0, 0.0};
     if (num_tiles <= 0 || pairs <= 0) return r;
     const int waves = (num_tiles + pairs - 1) / pairs;
+    r.waves = waves;
     const int rem = num_tiles - (waves - 1) * pairs;
-    int S = pairs / rem;
-    if (S > MAX_SPLITS) S = MAX_SPLITS;
-    const int min_kb = waves >= 2 ? 16 : 8;
-    while (S > 1 && k_blocks / S < min_kb) --S;
     if (waves < 2) {
+        int S = pairs / rem;
+        if (S > MAX_SPLITS) S = MAX_SPLITS;
+        while (S > 1 && k_blocks / S < 8) --S;
         if (S == 3) S = 2;   // clusters of 2S CTAs: 4 or 8
         if (S == 4 && num_tiles > caps.max8) S = 2;
         if (S == 2 && num_tiles > caps.max4) S = 1;
@@ -691,12 +808,34 @@ static TailSplit tail_split(int num_tiles, int k_blocks, int pairs, const Cluste
         r.full_tiles = 0;
         r.num_units = num_tiles * S;
         r.cluster = 1;
+        r.waves = 1.0 / S;
         return r;
     }
-    if (S < 2) return r;
-    r.splits = S;
+    // Only for long k loops: a split tile costs its pieces a 128 KB partial
+    // write per CTA and the last piece the reads of the others, ~30 GB/s per
+    // SM while the pair's TMA traffic shares the port (~5 us per partial,
+    // scripts/trace_tf32.py, profiles/r02_streamk.txt) -- at K = 1024 (64
+    // k-blocks, ~34 us per tile) that ate the whole gain.
+    if (!streamk || rem == pairs || k_blocks < SK_MIN_TILE_KB) return r;
+    static const int force_workers = [] {   // LPY_TF32_SKW=n: n stream-K workers (diagnostics / A-B)
+        const char *e = getenv("LPY_TF32_SKW");
+        return e ? atoi(e) : 0;
+    }();
+    const long long iters = static_cast<long long>(rem) * k_blocks;
+    long long workers = pairs;
+    if (workers > static_cast<long long>(rem) * SK_MAX_PIECES) workers = static_cast<long long>(rem) * SK_MAX_PIECES;
+    if (workers > iters / SK_MIN_KB) workers = iters / SK_MIN_KB;
+    if (force_workers > rem && force_workers <= pairs && force_workers <= rem * SK_MAX_PIECES)
+        workers = force_workers;
+    const double tail = double(rem) / double(workers > 0 ? workers : 1);
+    if (workers <= rem || tail > 0.8) return r;
     r.full_tiles = (waves - 1) * pairs;
-    r.num_units = r.full_tiles + (num_tiles - r.full_tiles) * S;
+    r.sk_workers = int(workers);
+    r.sk_stride = pairs;
+    r.sk_iters = iters;
+    r.num_units = r.full_tiles + 2 * pairs;
+    // + the fix-up: the last piece of a tile re-reads its tile's partials
+    r.waves = (waves - 1) + tail + 0.05;
     return r;
 }
 
@@ -716,11 +855,7 @@ int choose_bn(int M, int N, int K, int pairs, const ClusterCaps &caps) {
         const int64_t tn = (N + bn - 1) / bn, tiles = tm * tn;
         const TailSplit ts = tail_split(int(tiles), kb, pairs, caps);
         const double kern = bn == 256 ? 1.0 : bn == 192 ? 0.86 : 0.69;
-        // whole-tile waves, then the split units' waves at 1/S of a tile each
-        const int64_t full_waves = (ts.full_tiles + pairs - 1) / pairs;
-        const int64_t split_units = ts.num_units - ts.full_tiles;
-        const double split_waves = double((split_units + pairs - 1) / pairs) / ts.splits;
-        return (double(full_waves) + split_waves) * bn / kern * double(tn * bn) / double(N);
+        return ts.waves * bn / kern * double(tn * bn) / double(N);
     };
     int best = 256;
     double best_cost = cost(256);
@@ -743,7 +878,7 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, const ClusterCap
     else     e = make_tmap_2d(&tb, p.B, p.K, p.N, p.ldb, BK, BN_CTA, CU_TENSOR_MAP_SWIZZLE_64B);
     if (e != cudaSuccess) return e;
 
-    Params prm;
+    Params prm{};
     prm.M = p.M; prm.N = p.N; prm.K = p.K;
     prm.C = p.C; prm.ldc = p.ldc;
     prm.tiles_m = (p.M + BM * CG - 1) / (BM * CG);
@@ -754,17 +889,15 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, const ClusterCap
     prm.promote = kn.promote_kblocks > 0 ? kn.promote_kblocks : 8;   // 128 of K per TMEM partial
     prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
     prm.c_vec8 = ((reinterpret_cast<uintptr_t>(p.C) & 31) == 0) && (p.ldc % 8 == 0);
-    static const int l2hint = [] {   // LPY_L2HINT=0|1|2 (diagnostics / A-B)
-        const char *e = getenv("LPY_L2HINT");
-        return e ? atoi(e) : 0;
-    }();
-    prm.l2hint = l2hint;
     prm.trace = g_trace;
     {
         const TailSplit ts = tail_split(prm.num_tiles, prm.k_blocks, kn.num_sms / CG, caps);
         prm.splits = ts.splits;
         prm.full_tiles = ts.full_tiles;
         prm.num_units = ts.num_units;
+        prm.sk_workers = ts.sk_workers;
+        prm.sk_stride = ts.sk_stride;
+        prm.sk_iters = ts.sk_iters;
         prm.cluster_split = CG == 2 ? ts.cluster : 0;
         if (CG == 1 && ts.cluster) {   // (single-CTA diagnostics variant: no cluster split)
             prm.splits = 1;
@@ -785,15 +918,16 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, const ClusterCap
         else units = prm.num_units;
     }
     const int grid = units * CG;
-    if (prm.splits > 1 && !prm.cluster_split) {
+    if ((prm.splits > 1 && !prm.cluster_split) || prm.sk_workers > 0) {
         const int split_tiles = prm.num_tiles - prm.full_tiles;
-        const size_t ws_bytes = size_t(split_tiles) * prm.splits * CG * BM * BN * 4;
+        const size_t slots = prm.sk_workers > 0 ? size_t(2) * prm.sk_stride : size_t(split_tiles) * prm.splits;
+        const size_t ws_bytes = slots * CG * BM * BN * 4;
         char *buf = nullptr;
-        e = cudaMallocAsync(reinterpret_cast<void **>(&buf), ws_bytes + size_t(split_tiles) * CG * 4, s);
+        e = cudaMallocAsync(reinterpret_cast<void **>(&buf), ws_bytes + size_t(split_tiles) * CG * 8, s);
         if (e != cudaSuccess) return e;
         prm.ws = reinterpret_cast<float *>(buf);
         prm.sem = reinterpret_cast<int *>(buf + ws_bytes);
-        e = cudaMemsetAsync(prm.sem, 0, size_t(split_tiles) * CG * 4, s);
+        e = cudaMemsetAsync(prm.sem, 0, size_t(split_tiles) * CG * 8, s);
         if (e != cudaSuccess) { cudaFreeAsync(buf, s); return e; }
     }
 
@@ -811,6 +945,7 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, const ClusterCap
         Params q = prm;
         q.cluster_split = 0;
         q.splits = 1;
+        q.sk_workers = 0;
         q.full_tiles = q.num_units = q.num_tiles;
         const int g = CG * (q.num_units < kn.num_sms / CG ? q.num_units : kn.num_sms / CG);
         e = launch(q, g > 0 ? g : CG);

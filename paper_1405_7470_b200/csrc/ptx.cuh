@@ -393,6 +393,33 @@ __device__ __forceinline__ void ld_cg_v8(const float *p, float *v) {
                  : "memory");
 }
 
+// As ld_cg_v8 but NOT volatile and without a memory clobber, so the compiler
+// may batch and overlap these loads with one another (a volatile asm is kept
+// in program order against the adds that consume it, serialising a stream of
+// loads on their latency).  The caller must make the address depend on a
+// value produced after whatever synchronisation the data needs (see
+// opaque_zero), or the load could be hoisted above it.
+__device__ __forceinline__ void ld_cg_v8_nv(const float *p, float *v) {
+    asm("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+        : "l"(p));
+}
+// 0, produced at this point of the program (volatile + memory clobber: not
+// moved across barriers/fences), to anchor addresses of ld_cg_v8_nv loads.
+__device__ __forceinline__ uint32_t opaque_zero() {
+    uint32_t z;
+    asm volatile("mov.u32 %0, 0;" : "=r"(z)::"memory");
+    return z;
+}
+
+// Acquire load at GPU scope (a counter another CTA released with a fence +
+// atomic).
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // Programmatic dependent launch: wait until the grid this one depends on in
 // stream order has completed and its memory is visible (no-op when launched
 // without the programmatic-serialization attribute or after a plain kernel),

@@ -4,7 +4,7 @@
 averaged over CTAs: MMA thread waiting for transformed stages / for drained
 TMEM buffers, producer waiting for free stages, transform warp waiting for TMA.
 
-usage: python scripts/trace_tf32.py [n] [promote_kblocks]
+usage: python scripts/trace_tf32.py [n | M,N,K] [promote_kblocks]
 """
 import ctypes
 import os
@@ -22,10 +22,12 @@ lpy.library_path = lambda: TRACE
 lib = lpy.load_library()
 lib.lpy_trace_set_buffer.argtypes = [ctypes.c_void_p]
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+shape = sys.argv[1] if len(sys.argv) > 1 else "8192"
+M, N, K = (int(x) for x in shape.split(",")) if "," in shape else (int(shape),) * 3
+n = M
 promote = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-A = torch.randn(n, n, device="cuda")
-B = torch.randn(n, n, device="cuda")
+A = torch.randn(M, K, device="cuda")
+B = torch.randn(K, N, device="cuda")
 if os.environ.get("LA", "row") == "col":   # LA / LB = row|col: operand layouts
     A = A.t().contiguous().t()
 if os.environ.get("LB", "row") == "col":
@@ -35,7 +37,7 @@ opts.promote_kblocks = promote
 for _ in range(3):
     lpy.gemm(A, B, path="3xtf32", opts=opts)
 sms = torch.cuda.get_device_properties(0).multi_processor_count
-buf = torch.zeros(sms * 8 + 16 + 4 * sms, dtype=torch.int64, device="cuda")
+buf = torch.zeros(sms * 8 + 16 + 12 * sms, dtype=torch.int64, device="cuda")
 lib.lpy_trace_set_buffer(buf.data_ptr())
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
@@ -52,7 +54,7 @@ if tl[0]:
     print("CTA 0 timeline (us from entry):")
     for name, v in zip(ev, tl):
         print(f"  {name:44s} {(v - tl[0]) / 1e3 if v else float('nan'):8.2f}")
-ce4 = buf[grid * 8 + 16: grid * 8 + 16 + 4 * grid].view(grid, 4).double()
+ce4 = buf[grid * 8 + 16: grid * 8 + 16 + 12 * grid].view(grid, 12).double()
 ce = ce4[:, :2]
 if ce[0, 0] > 0:
     t0 = ce[:, 0].min()
@@ -66,12 +68,35 @@ if ce[0, 0] > 0:
         f0, f1 = (ce4[fx, 2] - t0) / 1e3, (ce4[fx, 3] - t0) / 1e3
         print(f"  fix-up CTAs: {int(fx.sum())}, start min/med/max {f0.min():.2f}/{f0.median():.2f}/{f0.max():.2f}, "
               f"loads done min/med/max {f1.min():.2f}/{f1.median():.2f}/{f1.max():.2f}, exit max {en[fx].max():.2f}")
+    mm = ce4[:, 4] > 0
+    if mm.any():
+        m1 = (ce4[mm, 4] - t0) / 1e3
+        print(f"  MMA loop done (leaders) min/med/max {m1.min():.2f}/{m1.median():.2f}/{m1.max():.2f}")
+    lp = ce4[:, 5] > 0
+    if lp.any():
+        l1 = (ce4[lp, 5] - t0) / 1e3
+        print(f"  last partial promoted min/med/max {l1.min():.2f}/{l1.median():.2f}/{l1.max():.2f}")
+    wt = ce4[:, 7] > 0
+    if wt.any():
+        w7 = (ce4[wt, 7] - t0) / 1e3
+        print(f"  fix-up: other pieces written min/med/max {w7.min():.2f}/{w7.median():.2f}/{w7.max():.2f}; "
+              f"reads (loads done - written) med/max {((ce4[wt, 3] - ce4[wt, 7]) / 1e3).median():.2f}/"
+              f"{((ce4[wt, 3] - ce4[wt, 7]) / 1e3).max():.2f}")
+    wr = ce4[:, 8] > 0
+    if wr.any():
+        a8, a9 = (ce4[wr, 8] - t0) / 1e3, (ce4[wr, 9] - t0) / 1e3
+        print(f"  writers: {int(wr.sum())}, ticket min/med/max {a8.min():.2f}/{a8.median():.2f}/{a8.max():.2f}, "
+              f"write time med/max {(a9 - a8).median():.2f}/{(a9 - a8).max():.2f}")
+    sk = ce4[:, 6] > 0
+    if sk.any():
+        s1 = (ce4[sk, 6] - t0) / 1e3
+        print(f"  first split piece's first MMA (leaders) min/med/max {s1.min():.2f}/{s1.median():.2f}/{s1.max():.2f}")
 t = buf[: sms * 8].view(sms, 8).double()
 lead = t[t[:, 0] > 0]
 names = ["mma_total", "mma_wait_ready", "mma_wait_acce", "prod_wait_empty", "xform_wait_full",
          "epi_wait_accf", "xform_busy", "epi_busy"]
 ms = e0.elapsed_time(e1)
-print(f"n={n} promote={promote or 'default'}: {ms:.3f} ms, {2 * n ** 3 / ms / 1e9:.1f} GFLOP/s")
+print(f"{M}x{N}x{K} promote={promote or 'default'}: {ms:.3f} ms, {2 * M * N * K / ms / 1e9:.1f} GFLOP/s")
 tot = lead[:, 0].mean().item()
 print(f"MMA thread cycles (mean over {lead.shape[0]} leader CTAs): {tot:.3e}")
 for i, nm in enumerate(names):

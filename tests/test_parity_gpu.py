@@ -215,8 +215,13 @@ def test_full_size_sampled(path, n, dist):
     rng = np.random.default_rng(n)
     edges = np.unique(np.concatenate([np.arange(0, n, 128), np.arange(127, n, 128),
                                       np.arange(0, n, 224) if n % 224 else [], [n - 1]])).astype(int)
-    ii = np.concatenate([np.repeat(edges[::4], 8), rng.integers(0, n, 3000)])
-    jj = np.concatenate([np.tile(edges[:8], len(edges[::4])), rng.integers(0, n, 3000)])
+    # tile-boundary rows x tile-boundary columns over the WHOLE of i and j (every
+    # fourth boundary on one axis against every boundary on the other, both
+    # ways; j = n-1 and i = n-1 included), plus random entries
+    r4, c4 = edges[::4], edges[1::4]
+    ii = np.concatenate([np.repeat(r4, len(edges)), np.repeat(edges, len(c4)), [n - 1], rng.integers(0, n, 3000)])
+    jj = np.concatenate([np.tile(edges, len(r4)), np.tile(c4, len(edges)), [n - 1], rng.integers(0, n, 3000)])
+    assert (n - 1) in set(jj[: len(r4) * len(edges)]) and jj.max() == n - 1
     Cref, D = oracle.gemm_elems(n, n, n, A.reshape(-1), n, 0, B.reshape(-1), n, 0, ii, jj)
     err = oracle.normalized_error(C[ii, jj], Cref, D)
     assert err <= TOL, err
@@ -480,3 +485,40 @@ def test_cluster_split_ragged_edges(path, M, N, K, la, lb, lc):
     o.num_ctas = 6
     C2, _ = run_gemm(A, B, la, lb, lc, ldc=synth.min_ld(M, N, lc) + 3, path=path, opts=o)
     assert np.array_equal(C, C2)
+
+
+@pytest.mark.parametrize("M,N,K,la,lb", [
+    (1024, 8192, 4096, 0, 0),    # the g = 8 row panel at K = 4096: 128 pair tiles on 74 pairs, 54 in the tail
+    (768, 6400, 4096, 0, 0),     # 75 tiles: one tail tile cut over 4 workers (the per-tile piece bound)
+    (1300, 4000, 4100, 1, 1),    # ragged M, N and K (257 k-blocks), column-major A and B: 96 tiles
+    (2560, 2304, 4100, 0, 1),    # 90 tiles, 16 in the tail: 4 pieces per tile, ragged K, column-major B
+])
+def test_stream_k_tail(M, N, K, la, lb):
+    """3xTF32 stream-K tail (gemm_3xtf32.cu tail_split): the last partial wave's
+    k-iterations are dealt out evenly to the CTA pairs, tiles are cut at
+    arbitrary k-blocks and their pieces summed in k order by the last to
+    finish.  Every element against a float64 library product, tile-boundary
+    rows against the oracle, and bitwise invariance under capped grids (the
+    decomposition follows the SM count, never opts.num_ctas).  Stream-K runs
+    for K >= 4096 (256 k-blocks) when it shortens the last wave by >= 20%."""
+    A, B = inputs(M, N, K, seed=M + N)
+    ref, pad_ok = run_gemm(A, B, la=la, lb=lb, path="3xtf32")
+    assert pad_ok
+    C64 = torch.from_numpy(A).double() @ torch.from_numpy(B).double()
+    D64 = torch.from_numpy(np.abs(A)).double() @ torch.from_numpy(np.abs(B)).double()
+    err = ((torch.from_numpy(ref).double() - C64).abs() / D64).max().item()
+    assert err <= TOL, err
+    rows = np.unique(np.clip(np.concatenate([np.arange(0, M, 128), np.arange(127, M, 128), [M - 1]]), 0, M - 1))
+    ii = np.repeat(rows, N)
+    jj = np.tile(np.arange(N), rows.size)
+    Cref, Dref = oracle.gemm_elems(M, N, K, np.ascontiguousarray(A).reshape(-1), K, 0,
+                                   np.ascontiguousarray(B).reshape(-1), N, 0, ii, jj)
+    assert oracle.normalized_error(ref[ii, jj], Cref, Dref) <= TOL
+    for ctas in (148, 100, 30, 2):
+        o = lpy.GemmOpts()
+        o.num_ctas = ctas
+        C, _ = run_gemm(A, B, la=la, lb=lb, path="3xtf32", opts=o)
+        assert np.array_equal(C, ref), ctas
+    for _ in range(3):                                    # repeatable (race detector)
+        C, _ = run_gemm(A, B, la=la, lb=lb, path="3xtf32")
+        assert np.array_equal(C, ref)
