@@ -182,6 +182,32 @@ def oracle_sample(n: int, seconds: float, dist_name: str, nthreads: int = 0):
     return gflops, dt, f"first {rows} rows of C for n={n} (all of B), float64 i-k-j loop", threads
 
 
+JSON_OUT = {"fd": None}
+
+
+def emit(line: dict) -> None:
+    """Print the one JSON line on the real stdout (saved before NCCL could
+    write to fd 1)."""
+    fd = JSON_OUT["fd"]
+    if fd is None:
+        print(json.dumps(line), flush=True)
+    else:
+        sys.stdout.flush()
+        os.write(fd, (json.dumps(line) + "\n").encode())
+
+
+def cpu_model() -> str | None:
+    """The host CPU's model name (lscpu's "Model name"), from /proc/cpuinfo."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.lower().startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle as it stands, timed on this box's host cores."""
     if rank != 0:
@@ -214,65 +240,57 @@ def run_reference(args, rank, world):
         "config": {"workload": f"n={n} square C=A*B, row-major (BASELINE config 4), "
                                f"bounded sample: {rows} rows of C per step"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------------- GPU arm
-def make_inputs(n, rank, world, chunks, device, owners=False, comm_world=None):
-    """This rank's A panel and the column blocks of B it holds before the step
-    (all of them on rank 0, or block c on rank c mod world with owners=True)."""
+def host_inputs(n, r0, r1, chunk_rows):
+    """Host (numpy) A panel rows [r0, r1) and the K-row chunks of B listed in
+    `chunk_rows` [(k0, k1), ...] (None: all of B) -- the seeded synthetic
+    inputs; every rank draws only what it holds."""
     import numpy as np
-    import torch
     import synth
-    from paper_1405_7470_b200.dist import block_owner, chunk_bounds, panel_bounds
-    r0, r1 = panel_bounds(n, world, rank)
-    A = torch.from_numpy(synth.matrix(r1 - r0, n, seed=0, matrix_id=synth.MATRIX_A, row0=r0)).to(device)
-    bounds = chunk_bounds(n, chunks)
-    blocks = []
-    cw = comm_world or world
-    for c, (c0, c1) in enumerate(bounds):
-        if rank == block_owner(c, cw, 0, owners):
-            blk = synth.matrix(n, c1 - c0, seed=0, matrix_id=synth.MATRIX_B, col0=c0)
-            blocks.append(torch.from_numpy(blk).to(device))
-        else:
-            blocks.append(torch.empty((n, c1 - c0), dtype=torch.float32, device=device))
-    C = torch.empty((r1 - r0, n), dtype=torch.float32, device=device)
-    return A, blocks, C, bounds, (r0, r1)
+    A = synth.matrix(r1 - r0, n, seed=0, matrix_id=synth.MATRIX_A, row0=r0)
+    if chunk_rows is None:
+        return A, synth.matrix(n, n, seed=0, matrix_id=synth.MATRIX_B)
+    B = np.full((n, n), np.nan, dtype=np.float32)
+    for k0, k1 in chunk_rows:
+        B[k0:k1] = synth.matrix(k1 - k0, n, seed=0, matrix_id=synth.MATRIX_B, row0=k0)
+    return A, B
 
 
 def time_path(args, path, rank, world, device, dist_on):
+    """Device-resident step.  N = 1: one lpy_gemm_f32 call.  N > 1 (or
+    --force-dist): the fused row-panel step, dist.gemm_rowpanel -- B broadcast
+    from its owner(s) in K-row chunks on a communication stream while ONE
+    K-gated product per rank consumes the chunks as they land."""
     import torch
     import paper_1405_7470_b200 as lpy
-    from paper_1405_7470_b200.dist import (choose_chunks, chunk_grid, chunk_streams, chunk_tile_n, panel_bounds,
-                                          rowpanel_gemm)
+    from paper_1405_7470_b200.dist import (choose_kchunks, gemm_rowpanel, kchunk_bounds, owned_chunks,
+                                          panel_bounds, panel_opts, chunk_owner)
     n = args.n
     pw = args.emulate_ranks if (args.emulate_ranks and world == 1) else world   # panel split
-    r0_, r1_ = panel_bounds(n, pw, rank)
+    r0, r1 = panel_bounds(n, pw, rank)
+    rows = r1 - r0
     sms = torch.cuda.get_device_properties(device).multi_processor_count
-    chunks = (args.chunks or choose_chunks(r1_ - r0_, n, sms)) if dist_on else 1
     owners = args.bcast == "owners"
-    A, blocks, C, bounds, (r0, r1) = make_inputs(n, rank, pw, chunks, device, owners, world)
-
-    def gemm_fn(a, b, c):
-        opts = None
-        if dist_on and len(bounds) > 1:
-            opts = lpy.GemmOpts()
-            opts.num_ctas = chunk_grid(a.shape[0], b.shape[1], sms, path)
-            opts.tile_n = chunk_tile_n(path)
-        lpy.gemm(a, b, out=c, path=path, opts=opts)
-
-    comm = torch.cuda.Stream() if dist_on else None
-    cstreams = [torch.cuda.Stream() for _ in range(chunk_streams(r1 - r0, len(bounds)))] if dist_on else None
+    bounds = kchunk_bounds(n, args.chunks or choose_kchunks(rows, n, path)) if dist_on else [(0, n)]
+    mine = owned_chunks(len(bounds), world, rank, 0, owners) if dist_on else [0]
+    Ah, Bh = host_inputs(n, r0, r1, [bounds[c] for c in mine] if dist_on and world > 1 else None)
+    A = torch.from_numpy(Ah).to(device)
+    B = torch.from_numpy(Bh).to(device)
+    del Bh
+    C = torch.empty((rows, n), dtype=torch.float32, device=device)
 
     def step():
         if not dist_on:
-            lpy.gemm(A, blocks[0], out=C, path=path)
+            lpy.gemm(A, B, out=C, path=path)
         else:
-            rowpanel_gemm(A, blocks, C, bounds, gemm_fn=gemm_fn, comm_stream=comm, compute_streams=cstreams,
-                          owners=owners)
+            gemm_rowpanel(A, B, chunks=bounds, path=path, out=C, owners=owners, reserve_sms=args.reserve_sms,
+                          timings=False)
 
     for _ in range(args.warmup):
         step()
@@ -317,59 +335,116 @@ def time_path(args, path, rank, world, device, dist_on):
 
         total_ms = max_ms(total_ms)
         reps = max(3, min(args.steps, 10))
-        # the two halves of a step, each timed alone (max over ranks): B's broadcast
-        # (4*K*N bytes from rank 0) and this rank's panel products
-        from paper_1405_7470_b200.dist import block_owner
-        bcast_ms = timed(lambda: [dist.broadcast(b, src=block_owner(c, world, 0, owners))
-                                  for c, b in enumerate(blocks)], reps)
-        gemm_ms = timed(lambda: rowpanel_gemm(A, blocks, C, bounds, gemm_fn=gemm_fn, comm_stream=comm,
-                                              compute_streams=cstreams, broadcast=False), reps)
+        # the two halves of a step, each timed alone (max over ranks): B's
+        # chunked broadcast (4*K*N bytes from the owners) and this rank's
+        # product planned for the same SMs, ungated (bitwise the gated one)
+        opts = panel_opts(sms, args.reserve_sms)
+        bcast_ms = timed(lambda: [dist.broadcast(B[k0:k1], src=chunk_owner(c, world, 0, owners))
+                                  for c, (k0, k1) in enumerate(bounds)], reps)
+        gemm_ms = timed(lambda: lpy.gemm(A, B, out=C, path=path, opts=opts), reps)
         nbytes = 4 * n * n
         multi = {"total_ms": round(total_ms / args.steps, 4), "bcast_ms": round(bcast_ms, 4),
                  "gemm_ms": round(gemm_ms, 4), "bcast_bytes": nbytes,
-                 "bcast_algbw_gbs": round(nbytes / (bcast_ms * 1e-3) / 1e9, 1), "chunks": len(bounds)}
+                 "bcast_algbw_gbs": round(nbytes / (bcast_ms * 1e-3) / 1e9, 1), "chunks": len(bounds),
+                 "chunk_k": bounds[0][1] - bounds[0][0], "plan_sms": opts.plan_sms,
+                 "reserve_sms": args.reserve_sms, "bcast": args.bcast}
         dist.barrier()
-    # sampled parity of this run's output against the oracle (rank 0 panel)
+        step()                      # the output parity checks below is a full step's
+        torch.cuda.synchronize()
+    # sampled parity of this run's output against the oracle, on EVERY rank
+    # (max over ranks): the reference regenerates A's panel and all of B from
+    # the seeded generator on the host, independent of the broadcast
     parity = None
-    if rank == 0 and not args.no_parity:
-        parity = sampled_parity(A, blocks, bounds, C, n, r0)
-    _, chosen = lpy.lpy_select_path(r1 - r0, n, n, lpy.PATHS[path])
+    if not args.no_parity:
+        parity = sampled_parity(Ah, C, n, r0)
+        if dist_on:
+            import torch.distributed as dist
+            t = torch.tensor([parity], device=device, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            parity = float(t.item())
+    _, chosen = lpy.lpy_select_path(rows, n, n, lpy.PATHS[path])
+    launches = 1 + (len(bounds) if dist_on else 0)      # the product (+ one signal kernel per chunk)
     return {"total_ms": total_ms, "kernel_ms": kernel_ms, "clocks": clk.summary(), "parity": parity,
-            "path": {1: "ffma", 2: "3xtf32"}[chosen], "launches_per_step": len(bounds), "chunks": len(bounds),
+            "path": {1: "ffma", 2: "3xtf32"}[chosen], "launches_per_step": launches, "chunks": len(bounds),
             "multi": multi}
 
 
-def sampled_parity(A, blocks, bounds, C, n, r0, count=512):
+_B_HOST = {}
+
+
+def sampled_parity(Ah, C, n, r0, count=512):
+    """Max normalised error of `count` sampled elements of this rank's C
+    panel plus its first/last rows at every 256-column tile boundary, against
+    the float64 oracle on regenerated inputs."""
     import numpy as np
     import oracle
-    rng = np.random.default_rng(0)
-    rows = A.shape[0]
-    ii = rng.integers(0, rows, count)
-    jj = rng.integers(0, n, count)
-    Ah = A.cpu().numpy().reshape(-1)
-    Bh = np.concatenate([b.cpu().numpy() for b in blocks], axis=1).reshape(-1)
+    import synth
+    if n not in _B_HOST:
+        _B_HOST.clear()
+        _B_HOST[n] = synth.matrix(n, n, seed=0, matrix_id=synth.MATRIX_B).reshape(-1)
+    Bh = _B_HOST[n]
+    rng = np.random.default_rng(r0)
+    rows = Ah.shape[0]
+    edges = np.array(sorted({c for t in range(0, n, 256) for c in (t, t + 255) if c < n} | {n - 1}))
+    ii = np.concatenate([rng.integers(0, rows, count), np.zeros(edges.size, np.int64),
+                         np.full(edges.size, rows - 1)])
+    jj = np.concatenate([rng.integers(0, n, count), edges, edges])
     Ch = C.cpu().numpy()
-    Cref, D = oracle.gemm_elems(rows, n, n, Ah, n, 0, Bh, n, 0, ii, jj)
+    Cref, D = oracle.gemm_elems(rows, n, n, Ah.reshape(-1), n, 0, Bh, n, 0, ii, jj)
     return oracle.normalized_error(Ch[ii, jj], Cref, D)
 
 
-def time_e2e(args, path, rank, world, device):
-    """Same product end to end through lpy_gemm_f32_host: pinned host A panel
-    and B in, host C panel out, copies inside the timed region."""
+def time_e2e(args, path, rank, world, device, dist_on):
+    """The same step end to end from pinned HOST buffers through the public
+    API, copies inside the timed region.  N = 1: lpy_gemm_f32_host (A, B up,
+    C down).  N > 1: dist.gemm_rowpanel_host -- each rank uploads its A panel
+    and only the K-row chunks of B it owns (1/g of B), the chunks are broadcast
+    over NCCL as they land, the gated product consumes them, and each rank
+    downloads its C panel: 4(MK + KN) bytes up and 4MN down in total, not
+    g times B.  At world 1 with --force-dist --emulate-ranks g: rank 0's share
+    of a g-rank step (its own chunks only; a diagnostic, not a bench value)."""
     import torch
     import paper_1405_7470_b200 as lpy
     import synth
-    from paper_1405_7470_b200.dist import panel_bounds
+    from paper_1405_7470_b200.dist import (HostWorkspace, choose_kchunks, gemm_rowpanel_host, kchunk_bounds,
+                                          owned_chunks, panel_bounds)
     n = args.n
-    r0, r1 = panel_bounds(n, world, rank)
-    A = torch.from_numpy(synth.matrix(r1 - r0, n, seed=0, matrix_id=0, row0=r0)).pin_memory()
-    B = torch.from_numpy(synth.matrix(n, n, seed=0, matrix_id=1)).pin_memory()
-    C = torch.empty((r1 - r0, n), dtype=torch.float32).pin_memory()
-    s = torch.cuda.current_stream()
+    emul = args.emulate_ranks if (args.emulate_ranks and world == 1 and dist_on) else None
+    pw = emul or world
+    r0, r1 = panel_bounds(n, pw, rank)
+    rows = r1 - r0
+    A = torch.from_numpy(synth.matrix(rows, n, seed=0, matrix_id=0, row0=r0)).pin_memory()
     steps = max(1, min(args.steps, args.e2e_steps))
+    if not dist_on:
+        B = torch.from_numpy(synth.matrix(n, n, seed=0, matrix_id=1)).pin_memory()
+        C = torch.empty((rows, n), dtype=torch.float32).pin_memory()
+        s = torch.cuda.current_stream()
 
-    def step():
-        lpy.gemm_host(r1 - r0, n, n, A, n, 0, B, n, 0, C, n, 0, path=path, stream=s)
+        def step():
+            lpy.gemm_host(rows, n, n, A, n, 0, B, n, 0, C, n, 0, path=path, stream=s)
+            return 4 * (rows * n + n * n), 4 * rows * n
+    else:
+        # host buffers: every rank uploads only the K-row chunks it owns (c mod
+        # N), so B crosses PCIe once in total, then NVLink (owners broadcast)
+        owners = True
+        bounds = kchunk_bounds(n, args.chunks or choose_kchunks(rows, n, path))
+        mine = owned_chunks(len(bounds), pw, rank, 0, owners)
+        _, Bh = host_inputs(n, r0, r1, [bounds[c] for c in mine] if (world > 1 or emul) else None)
+        B = torch.from_numpy(Bh).pin_memory()
+        del Bh
+        C = torch.empty((rows, n), dtype=torch.float32).pin_memory()
+        ws = HostWorkspace()
+        if emul:
+            # the chunks rank 0 does not own are "delivered by its peers": put
+            # them in the workspace once, outside the timed region
+            Bfull = torch.from_numpy(synth.matrix(n, n, seed=0, matrix_id=1))
+            ws.get("B", (n, n), torch.device("cuda", torch.cuda.current_device())).copy_(Bfull)
+            del Bfull
+
+        def step():
+            info = gemm_rowpanel_host(A, B, C, chunks=bounds, path=path, owners=owners,
+                                      reserve_sms=args.reserve_sms, workspace=ws, emulate_world=emul)
+            return info["h2d_bytes"], info["d2h_bytes"]
 
     step()
     torch.cuda.synchronize()
@@ -379,19 +454,25 @@ def time_e2e(args, path, rank, world, device):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(steps):
-        step()
+        h2d, d2h = step()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
+    h2d_rank = h2d
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    h2d = 4 * ((r1 - r0) * n + n * n) * world
-    d2h = 4 * (r1 - r0) * n * world
-    return {"value": 2.0 * n ** 3 / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": ms}
+        t = torch.tensor([h2d, d2h], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        h2d, d2h = int(t[0].item()), int(t[1].item())
+    flops = 2.0 * n ** 3 / (pw if emul else 1)
+    out = {"value": flops / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": ms, "h2d_bytes_rank0": h2d_rank}
+    if emul:
+        out["emulated_rank0_of"] = emul
+    return out
 
 
 def time_cublas_context(args, device):
@@ -552,10 +633,12 @@ def main():
     ap.add_argument("--n", type=int, default=8192)
     ap.add_argument("--path", default="auto", choices=["auto", "ffma", "3xtf32"])
     ap.add_argument("--also", default="ffma", help="secondary path to report ('' for none)")
-    ap.add_argument("--chunks", type=int, default=0, help="B column blocks for N>1 (0 = ~1 wave each)")
+    ap.add_argument("--chunks", type=int, default=0, help="K-row chunks of B for N>1 (0 = dist.choose_kchunks)")
     ap.add_argument("--bcast", default="root", choices=["root", "owners"],
                     help="N>1: B starts on rank 0 and is broadcast (north_star), or starts sharded by "
-                         "column blocks and each owner broadcasts its blocks")
+                         "K-row chunks (chunk c on rank c mod N) and each owner broadcasts its chunks")
+    ap.add_argument("--reserve-sms", type=int, default=8,
+                    help="N>1: SMs the gated product leaves to the broadcast (dist.RESERVE_SMS)")
     ap.add_argument("--emulate-ranks", type=int, default=0,
                     help="diagnostics at N=1 with --force-dist: rank 0's panel of an N-rank split (not a bench value)")
     ap.add_argument("--force-dist", action="store_true",
@@ -594,20 +677,21 @@ def main():
             os.environ.setdefault("MASTER_PORT", "29533")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        # NCCL prints its version banner to stdout at communicator creation when
-        # NCCL_DEBUG=VERSION (this image's default): send fd 1 to stderr until the
-        # communicator exists, so stdout carries only the JSON line
+        # NCCL's INIT lines (rank / nRanks / transport per communicator) go to stderr,
+        # where the launcher's rank check reads them
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        # NCCL prints its debug lines (and the version banner) to stdout, at
+        # communicator creation and destruction: fd 1 goes to stderr for the
+        # whole distributed run and the JSON line is written to the saved
+        # stdout, so stdout carries only that line
         sys.stdout.flush()
-        saved = os.dup(1)
+        JSON_OUT["fd"] = os.dup(1)
         os.dup2(2, 1)
-        try:
-            dist.init_process_group("nccl", device_id=device)
-            dist.barrier()
-            torch.cuda.synchronize()
-        finally:
-            sys.stdout.flush()
-            os.dup2(saved, 1)
-            os.close(saved)
+        dist.init_process_group("nccl", device_id=device)
+        dist.barrier()
+        torch.cuda.synchronize()
 
     main_path = args.path
     if main_path == "auto":
@@ -617,7 +701,7 @@ def main():
     also = None
     if args.also and args.also != main_path:
         also = time_path(args, args.also, rank, world, device, dist_on)
-    e2e = None if args.no_e2e else time_e2e(args, main_path, rank, world, device)
+    e2e = None if args.no_e2e else time_e2e(args, main_path, rank, world, device, dist_on)
     sax = time_saxpy(args, device) if (args.saxpy_n > 0 and rank == 0 and not dist_on) else None
     coul = time_coulomb(args, device) if (args.coulomb_n > 0 and rank == 0 and not dist_on) else None
     ctx = time_cublas_context(args, device) if (not args.no_context and rank == 0 and not dist_on) else None
@@ -634,7 +718,7 @@ def main():
             bound, peak, note = roofline_peak(path)
             if not dist_on:        # one GEMM launch per step: its CUDA-event time
                 kms, kflops = statistics.mean(r["kernel_ms"]), flops
-            else:                  # rank 0's panel products without the broadcast
+            else:                  # rank 0's panel product alone (ungated, same plan), no broadcast
                 kms, kflops = r["multi"]["gemm_ms"], flops / world
             achieved = kflops / (kms * 1e-3) / 1e12
             traffic, tsrc = profile_traffic(path, n)
@@ -644,10 +728,11 @@ def main():
                     "peak_note": note, "kernel_ms_mean": round(kms, 4)}
 
         cpu = None
-        if not args.no_cpu and world == 1:
+        if not args.no_cpu:
+            # rank 0's host cores at every N (the other ranks wait at the final barrier)
             gf, dt, sample, threads = oracle_sample(n, args.cpu_seconds, "uniform")
             cpu = {"value": round(gf, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
-                   "sample": sample, "seconds": round(dt, 2)}
+                   "sample": sample, "seconds": round(dt, 2), "cpu_model": cpu_model()}
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
@@ -659,7 +744,7 @@ def main():
             "data": "synthetic: seeded SplitMix64 uniform[-1,1) fp32 on a 2^-23 grid",
             "config": {"workload": f"n={n} square fp32 C=A*B, row-major A/B/C (BASELINE config 4)",
                        "path": res["path"], "M": n, "N": n, "K": n,
-                       "parallelism": f"rowpanel{world}" + (f"+nccl_bcast_B_chunks{res['chunks']}" + ("_owners" if args.bcast == "owners" else "") if dist_on else ""),
+                       "parallelism": f"rowpanel{world}" + (f"+nccl_bcast_B_kchunks{res['chunks']}" + ("_owners" if args.bcast == "owners" else "") + "+gated_product" if dist_on else ""),
                        "l2": "inputs larger than L2 (A, B, C 268 MB each > 126 MB), no flush"},
             "roofline": roof(res, res["path"]),
             "cpu_baseline": cpu,
@@ -682,7 +767,7 @@ def main():
             line["alt_path"] = {"path": also["path"], "value": round(flops / (ams * 1e-3) / 1e9, 1),
                                 "ms_per_step": round(ams, 4), "roofline": roof(also, also["path"]),
                                 "parity_sampled_max_norm_err": also["parity"], "clocks": also["clocks"]}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist_on:
         import torch.distributed as dist
         dist.barrier()

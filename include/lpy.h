@@ -74,7 +74,7 @@
 extern "C" {
 #endif
 
-#define LPY_VERSION 4
+#define LPY_VERSION 5
 
 typedef enum { LPY_ROW_MAJOR = 0, LPY_COL_MAJOR = 1 } lpy_layout;
 
@@ -129,7 +129,15 @@ typedef struct lpy_gemm_opts {
                              /* grid (num_ctas); a different tile width can change   */
                              /* the k-split of under-filled grids and so the last    */
                              /* bits (always within the 1e-5 bound)                  */
-    int32_t reserved[4];     /* must be 0                                            */
+    int32_t plan_sms;        /* SMs the schedule is planned for: 0 = the device's    */
+                             /* (all of them), else 1..device SMs.  Sets the tile    */
+                             /* width, the split-K / stream-K decomposition and the  */
+                             /* default grid; the result depends on it (like tile_n) */
+                             /* but never on num_ctas.  A product sharing the GPU    */
+                             /* with concurrent work (the row-panel product beside   */
+                             /* its broadcast, lpy_gemm_f32_gated) plans for the SMs */
+                             /* it will actually get                                 */
+    int32_t reserved[3];     /* must be 0                                            */
 } lpy_gemm_opts;
 
 /* C := A * B on the device, enqueued on `stream` (see header comment).
@@ -146,6 +154,69 @@ lpy_status lpy_gemm_f32_ex(int64_t M, int64_t N, int64_t K,
                            const float *B, int64_t ldb, lpy_layout layout_b,
                            float *C, int64_t ldc, lpy_layout layout_c,
                            void *stream, lpy_path path, const lpy_gemm_opts *opts);
+
+/* ---------------------------------------------------------------- K-gated product
+ * The row-panel product of the multi-GPU step (BASELINE north_star: C's row
+ * panels sharded over the GPUs, B broadcast once over NVLink)
+ * starts while B is still arriving.  Every output tile walks K in order, so
+ * the k-th rows of B are needed only when the tiles reach k: B is broadcast in
+ * chunks of K rows (contiguous in row-major B) and ONE persistent product
+ * consumes each chunk as soon as it has landed -- the paper's reduction
+ * sum(k, a[i,k]*b[k,j]) with its k loop split into chunks
+ * (split_iname) whose prefetch (add_prefetch) waits for
+ * the chunk's arrival.
+ *
+ * lpy_kgate describes the arrival flags: chunk c = k in [c*chunk_k,
+ * min(K, (c+1)*chunk_k)), published by setting flags[c] to `epoch` (e.g. with
+ * lpy_kgate_signal after the chunk's broadcast, stream-ordered).  The product
+ * reads NO element of A or B with k in chunk c before (int32_t)(flags[c] -
+ * epoch) >= 0, i.e. flags compare wrap-aware, so a caller reuses one flag
+ * array across steps by raising the epoch (no reset).  Chunks must be published
+ * in increasing c (the kernels poll the next chunk only).
+ *   flags      : device memory of the current device, ceil(K / chunk_k) words,
+ *                owned by the caller, read (never written) by the product.
+ *   chunk_k    : K indices per chunk, >= 32 (a k-block of 32 spans at most two
+ *                chunks) and <= 2^31 - 1024.
+ *   epoch      : the value that marks a chunk ready in this call.
+ *   timeout_ms : a chunk not ready this long after the kernel first polls it
+ *                traps the kernel (a deadlock detector: the error surfaces at
+ *                the next synchronisation as a CUDA launch failure and the
+ *                context is lost); 0 = 10000 ms.
+ * SCHEDULING CONTRACT.  The product spins on the flags while occupying its
+ * grid, so whatever sets them (the broadcast's NCCL kernels and the signal
+ * kernel) must be able to run beside it: plan the product for fewer SMs than
+ * the device has (opts.plan_sms; dist.py leaves 8 free) or set the flags from
+ * a copy engine / the host.  Every kernel that sets flags must also be LOADED
+ * before the product is launched: under CUDA's lazy module loading a kernel's
+ * first launch loads its code and waits for the device, i.e. for the spinning
+ * product (this call loads lpy_kgate_signal's kernel itself; a caller's own
+ * kernels -- NCCL's included -- must have run once, or be enqueued before the
+ * product as dist.py does).  Operands that would need the aligned repack
+ * (base not 16-byte aligned or ld not a multiple of 4) are LPY_ERR_NOT_SUPPORTED
+ * here: the repack would read them before they arrive.  Otherwise the
+ * arguments, errors and result are those of lpy_gemm_f32_ex with the same opts
+ * (bitwise: the gate changes when operands are read, not the arithmetic). */
+typedef struct lpy_kgate {
+    const uint32_t *flags;
+    int64_t chunk_k;
+    uint32_t epoch;
+    uint32_t timeout_ms;
+} lpy_kgate;
+
+lpy_status lpy_gemm_f32_gated(int64_t M, int64_t N, int64_t K,
+                              const float *A, int64_t lda, lpy_layout layout_a,
+                              const float *B, int64_t ldb, lpy_layout layout_b,
+                              float *C, int64_t ldc, lpy_layout layout_c,
+                              void *stream, lpy_path path, const lpy_gemm_opts *opts,
+                              const lpy_kgate *gate);
+
+/* Enqueue on `stream`: once all work before it in the stream has completed,
+ * *flag := value with release semantics at GPU scope (the writes of that
+ * earlier work -- e.g. a broadcast's received bytes -- are visible to a
+ * product that acquires the flag).  flag: device memory of the current
+ * device, 4-byte aligned (LPY_ERR_NULL_POINTER / LPY_ERR_MISALIGNED).  One
+ * 32-thread kernel launch; needs one free SM while a gated product runs. */
+lpy_status lpy_kgate_signal(uint32_t *flag, uint32_t value, void *stream);
 
 /* End-to-end variant on HOST buffers: copies the logical extents of A and B to
  * device scratch (stream-ordered, repacked to 16-byte-aligned leading

@@ -26,6 +26,7 @@ __all__ = [
     "lpy_gemm_f32_host", "lpy_select_path", "lpy_status_string", "lpy_last_cuda_error",
     "lpy_version", "gemm", "operand_layout", "gemm_host", "lpy_saxpy_f32", "lpy_saxpy_f32_host",
     "saxpy", "saxpy_host", "lpy_coulomb_f32", "lpy_coulomb_f32_host", "coulomb", "coulomb_host",
+    "KGate", "lpy_gemm_f32_gated", "lpy_kgate_signal", "kgate_signal",
 ]
 
 ROW_MAJOR = 0
@@ -47,7 +48,13 @@ def library_path() -> str:
 class GemmOpts(ctypes.Structure):
     _fields_ = [("num_ctas", ctypes.c_int32), ("raster_group", ctypes.c_int32),
                 ("promote_kblocks", ctypes.c_int32), ("tile_n", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("plan_sms", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+
+
+class KGate(ctypes.Structure):
+    """lpy_kgate: arrival flags of a product whose operands arrive in chunks of K."""
+    _fields_ = [("flags", ctypes.c_void_p), ("chunk_k", ctypes.c_int64), ("epoch", ctypes.c_uint32),
+                ("timeout_ms", ctypes.c_uint32)]
 
 
 class LpyError(RuntimeError):
@@ -76,6 +83,10 @@ def load_library():
         lib.lpy_gemm_f32.restype = i32
         lib.lpy_gemm_f32_ex.argtypes = gemm_args + [i32, ctypes.POINTER(GemmOpts)]
         lib.lpy_gemm_f32_ex.restype = i32
+        lib.lpy_gemm_f32_gated.argtypes = gemm_args + [i32, ctypes.POINTER(GemmOpts), ctypes.POINTER(KGate)]
+        lib.lpy_gemm_f32_gated.restype = i32
+        lib.lpy_kgate_signal.argtypes = [vp, ctypes.c_uint32, vp]
+        lib.lpy_kgate_signal.restype = i32
         lib.lpy_gemm_f32_host.argtypes = gemm_args + [i32]
         lib.lpy_gemm_f32_host.restype = i32
         lib.lpy_select_path.argtypes = [i64, i64, i64, i32, ctypes.POINTER(i32)]
@@ -111,6 +122,18 @@ def lpy_gemm_f32_ex(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc, layout_
     return load_library().lpy_gemm_f32_ex(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc,
                                           layout_c, stream, path,
                                           ctypes.byref(opts) if opts is not None else None)
+
+
+def lpy_gemm_f32_gated(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc, layout_c, stream=None,
+                       path=PATH_AUTO, opts: GemmOpts | None = None, gate: KGate | None = None) -> int:
+    return load_library().lpy_gemm_f32_gated(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc,
+                                             layout_c, stream, path,
+                                             ctypes.byref(opts) if opts is not None else None,
+                                             ctypes.byref(gate) if gate is not None else None)
+
+
+def lpy_kgate_signal(flag, value, stream=None) -> int:
+    return load_library().lpy_kgate_signal(flag, value & 0xFFFFFFFF, stream)
 
 
 def lpy_gemm_f32_host(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc, layout_c, stream=None,
@@ -204,9 +227,11 @@ def _path_id(path) -> int:
     return PATHS[path] if isinstance(path, str) else int(path)
 
 
-def gemm(A, B, out=None, path="auto", stream=None, opts: GemmOpts | None = None):
-    """C = A @ B for fp32 CUDA tensors through lpy_gemm_f32_ex.  `out` may be
-    row- or column-major (any ld); it is overwritten."""
+def gemm(A, B, out=None, path="auto", stream=None, opts: GemmOpts | None = None, gate: KGate | None = None):
+    """C = A @ B for fp32 CUDA tensors through lpy_gemm_f32_ex (or, with a
+    `gate`, lpy_gemm_f32_gated: operands read only as their K chunks are
+    flagged ready).  `out` may be row- or column-major (any ld); it is
+    overwritten."""
     import torch
     if A.dtype != torch.float32 or B.dtype != torch.float32:
         raise TypeError("lpy.gemm is fp32 in, fp32 out (PAPER.md P:362-365)")
@@ -233,12 +258,33 @@ def gemm(A, B, out=None, path="auto", stream=None, opts: GemmOpts | None = None)
         raise ValueError("out must be row- or column-major")
     lib = _lib or load_library()
     po = ctypes.byref(opts) if opts is not None else None
+    if gate is not None:
+        pg = ctypes.byref(gate)
+        st = _on_device((A, B, out), stream, lambda sh: lib.lpy_gemm_f32_gated(
+            M, N, K, A.data_ptr(), la[1], la[0], B.data_ptr(), lb[1], lb[0], out.data_ptr(), lc[1], lc[0], sh,
+            _path_id(path), po, pg))
+        if st != 0:
+            raise LpyError(st, "lpy_gemm_f32_gated")
+        return out
     st = _on_device((A, B, out), stream, lambda sh: lib.lpy_gemm_f32_ex(
         M, N, K, A.data_ptr(), la[1], la[0], B.data_ptr(), lb[1], lb[0], out.data_ptr(), lc[1], lc[0], sh,
         _path_id(path), po))
     if st != 0:
         raise LpyError(st, "lpy_gemm_f32_ex")
     return out
+
+
+def kgate_signal(flags, index, value, stream=None):
+    """flags[index] := value (uint32, release) once `stream`'s earlier work is
+    done, through lpy_kgate_signal.  `flags` is a CUDA int32 tensor (the flag
+    words; torch has no uint32 arithmetic, the bits are the same)."""
+    import torch
+    if flags.dtype != torch.int32 or not flags.is_cuda or flags.dim() != 1 or not 0 <= index < flags.shape[0]:
+        raise ValueError("flags must be a 1-D int32 CUDA tensor and index within it")
+    ptr = flags.data_ptr() + 4 * index
+    st = _on_device((flags,), stream, lambda sh: lpy_kgate_signal(ptr, int(value), sh))
+    if st != 0:
+        raise LpyError(st, "lpy_kgate_signal")
 
 
 def gemm_host(M, N, K, A, lda, la, B, ldb, lb, C, ldc, lc, path="auto", stream=None):

@@ -28,7 +28,7 @@ LIB = os.path.join(PKG, "liblpy.so")
 PROBE_LIB = os.path.join(PKG, "liblpy_probe.so")
 TRACE_LIB = os.path.join(PKG, "liblpy_trace.so")
 
-SOURCES = ["lpy_api.cu", "gemm_ffma.cu", "gemm_3xtf32.cu", "repack.cu", "saxpy.cu", "coulomb.cu"]
+SOURCES = ["lpy_api.cu", "gemm_ffma.cu", "gemm_3xtf32.cu", "repack.cu", "saxpy.cu", "coulomb.cu", "kgate.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}",
                      "-Xptxas", "-v"]
@@ -41,7 +41,7 @@ OBJECTS = [(os.path.splitext(s)[0], s, []) for s in SOURCES] + [
 LIBS = [
     (LIB, [os.path.splitext(s)[0] for s in SOURCES]),
     (PROBE_LIB, ["probe_tcgen05"]),
-    (TRACE_LIB, ["lpy_api", "gemm_ffma", "gemm_3xtf32_trace", "repack", "saxpy", "coulomb"]),
+    (TRACE_LIB, ["lpy_api", "gemm_ffma", "gemm_3xtf32_trace", "repack", "saxpy", "coulomb", "kgate"]),
 ]
 
 

@@ -102,6 +102,7 @@ struct Params {
     int cluster_split;
     float *ws;          // [(num_units - full_tiles)][CG][BM x BN] partial tiles
     int *sem;           // 2 x [(num_tiles - full_tiles)][CG] ticket / written counters, zero on entry and exit
+    KGate gate;         // operands arriving in chunks of K (lpy_kgate): the producer waits per k-block
 };
 
 // Stream-K: the worker whose iteration range contains tail iteration x
@@ -330,6 +331,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (lane == 0) {
                 int s = 0;
                 uint32_t ph = 0;
+                int gready = -1;                           // K-gate: chunks known ready
+                int glimit = kgate_limit0(p.gate);         // ... and the first k-block they do not cover
                 for (int u = unit0; u < p.num_units; u += units) {
                     int t, kb0, kb1, su, tm, tn;
                     unit_range(u, p, t, kb0, kb1, su);
@@ -337,6 +340,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const int m0 = tm * (BM * CG) + rank * BM;
                     const int n0 = tn * BN + rank * C_::BN_CTA;
                     for (int kb = kb0; kb < kb1; ++kb) {
+                        // (before the stage wait: off the critical path when the ring is full)
+                        if (kb >= glimit) glimit = kgate_admit(p.gate, gready, kb, BK, p.K);
                         TR_T0(t_w);
                         mbar_wait(&empty[s], ph ^ 1);
                         TR_ADD(3, t_w);
@@ -758,7 +763,7 @@ static long long *g_trace = nullptr;   // set by lpy_trace_set_buffer (diagnosti
 //    + 1, >= 16 k-blocks per worker), so the last wave takes rem / P' of a
 //    tile instead of a whole one -- a fractional split (the paper's "separate
 //    code for edge and corner cases").  Used when it shortens the
-//    last wave by >= 20% and K >= 4096.  (Round 1 cut the tail tiles into S = floor(pairs /
+//    last wave by >= 10% and K >= 4096.  (Round 1 cut the tail tiles into S = floor(pairs /
 //    rem) equal slices: at 128 tiles on 74 pairs, S = 1, no gain.)
 //  * a single under-filled wave (tiles < pairs, e.g. n = 1024): every tile is
 //    cut into S = 2 or 4 k-slices (S * tiles <= pairs, >= 8 k-blocks each)
@@ -828,7 +833,11 @@ static TailSplit tail_split(int num_tiles, int k_blocks, int pairs, const Cluste
     if (force_workers > rem && force_workers <= pairs && force_workers <= rem * SK_MAX_PIECES)
         workers = force_workers;
     const double tail = double(rem) / double(workers > 0 ? workers : 1);
-    if (workers <= rem || tail > 0.8) return r;
+    static const double max_tail = [] {     // LPY_TF32_SK_TAIL (A/B): largest tail worth splitting
+        const char *e = getenv("LPY_TF32_SK_TAIL");
+        return e ? atof(e) : 0.9;
+    }();
+    if (workers <= rem || tail > max_tail) return r;
     r.full_tiles = (waves - 1) * pairs;
     r.sk_workers = int(workers);
     r.sk_stride = pairs;
@@ -890,6 +899,7 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, const ClusterCap
     prm.c_vec = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && (p.ldc % 4 == 0);
     prm.c_vec8 = ((reinterpret_cast<uintptr_t>(p.C) & 31) == 0) && (p.ldc % 8 == 0);
     prm.trace = g_trace;
+    prm.gate = kn.gate;
     {
         const TailSplit ts = tail_split(prm.num_tiles, prm.k_blocks, kn.num_sms / CG, caps);
         prm.splits = ts.splits;
@@ -1005,7 +1015,7 @@ cudaError_t launch_3xtf32(const Problem &p, const Knobs &kn, cudaStream_t s) {
         const char *e = getenv("LPY_TF32_CG");
         return (e && e[0] == '1') ? 1 : 2;
     }();
-    const tf32::ClusterCaps caps = tf32::cluster_caps(kn.num_sms);
+    const tf32::ClusterCaps caps = tf32::cluster_caps(kn.dev_sms);
     if (cg == 1) return tf32::launch_cg<1, 256>(p, kn, caps, s);
     // LPY_TF32_BN=128|192|256 forces the tile width (diagnostics / A-B comparison).
     static const int force_bn = [] {

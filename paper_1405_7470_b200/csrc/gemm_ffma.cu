@@ -85,6 +85,7 @@ struct Params {
     // shared memory (no ws, no fix-up kernel)
     int cluster_split;
     int ws_stride;   // float4 stride between a thread's partial float4s: 256 (interleaved) or 1 (LPY_FFMA_PARTIAL=contig, A/B)
+    KGate gate;      // operands arriving in chunks of K (lpy_kgate): the producer waits per k-block
 };
 
 __device__ __forceinline__ void unit_range(int u, const Params &p, int &t, int &kb0, int &kb1) {
@@ -219,12 +220,15 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
                 tma_prefetch_desc(&tmB);
                 int stage = 0;
                 uint32_t phase = 0;
+                int gready = -1;                           // K-gate: chunks known ready
+                int glimit = kgate_limit0(p.gate);         // ... and the first k-block they do not cover
                 for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
                     int t, kb0, kb1, tm, tn;
                     unit_range(u, p, t, kb0, kb1);
                     tile_coords(t, p, tm, tn);
                     const int m0 = tm * BM, n0 = tn * BN;
                     for (int kb = kb0; kb < kb1; ++kb) {
+                        if (kb >= glimit) glimit = kgate_admit(p.gate, gready, kb, BK, p.K);
                         mbar_wait_sleep(&empty[stage], phase ^ 1, 2000);
                         mbar_arrive_expect_tx(&full[stage], G::TMA_BYTES);
                         if constexpr (AK) tma_load_2d(raw_a(stage), &tmA, &full[stage], kb * BK, m0);
@@ -497,6 +501,7 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
         return (v && v[0] == 'c') ? 1 : CWARPS * 32;
     }();
     prm.ws_stride = ws_stride;
+    prm.gate = kn.gate;
     int grid = kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms;
     if (grid > prm.num_units) grid = prm.num_units;
     if (grid < 1) grid = 1;

@@ -76,7 +76,8 @@ lpy_status validate_all(int64_t M, int64_t N, int64_t K, const Operand &A, const
             return LPY_ERR_INVALID_VALUE;
         if (opts->tile_n != 0 && opts->tile_n != 128 && opts->tile_n != 192 && opts->tile_n != 256)
             return LPY_ERR_INVALID_VALUE;
-        for (int i = 0; i < 4; ++i)
+        if (opts->plan_sms < 0) return LPY_ERR_INVALID_VALUE;   // (upper bound: the device's, checked at launch)
+        for (int i = 0; i < 3; ++i)
             if (opts->reserved[i] != 0) return LPY_ERR_INVALID_VALUE;
     }
     lpy_status s;
@@ -272,13 +273,23 @@ lpy_status lpy_select_path(int64_t M, int64_t N, int64_t K, lpy_path requested, 
     return LPY_OK;
 }
 
-lpy_status lpy_gemm_f32_ex(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
-                           lpy_layout layout_a, const float *B, int64_t ldb, lpy_layout layout_b,
-                           float *C, int64_t ldc, lpy_layout layout_c, void *stream, lpy_path path,
-                           const lpy_gemm_opts *opts) {
+}  // extern "C"
+
+namespace {
+
+// lpy_gemm_f32_ex and lpy_gemm_f32_gated (gate == nullptr: ungated).
+lpy_status gemm_impl(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, lpy_layout layout_a,
+                     const float *B, int64_t ldb, lpy_layout layout_b, float *C, int64_t ldc,
+                     lpy_layout layout_c, void *stream, lpy_path path, const lpy_gemm_opts *opts,
+                     const lpy_kgate *gate) {
     Operand oa{A, M, K, lda, int(layout_a)}, ob{B, K, N, ldb, int(layout_b)}, oc{C, M, N, ldc, int(layout_c)};
     lpy_status st = validate_all(M, N, K, oa, ob, oc, int(path), opts);
     if (st != LPY_OK) return st;
+    if (gate) {
+        if (gate->flags == nullptr) return LPY_ERR_NULL_POINTER;
+        if (reinterpret_cast<uintptr_t>(gate->flags) & 3) return LPY_ERR_MISALIGNED;
+        if (gate->chunk_k < 32 || gate->chunk_k > kMaxDim) return LPY_ERR_INVALID_VALUE;
+    }
 
     // Column-major C: C^T (N x M, row-major, ld = ldc) = B^T A^T, where the
     // transpose of a stored matrix is the same memory with the other layout tag.
@@ -293,6 +304,7 @@ lpy_status lpy_gemm_f32_ex(int64_t M, int64_t N, int64_t K, const float *A, int6
 
     DeviceInfo dev;
     if ((st = device_info(dev)) != LPY_OK) return st;
+    if (opts && opts->plan_sms > dev.sms) return LPY_ERR_INVALID_VALUE;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e;
 
@@ -318,6 +330,7 @@ lpy_status lpy_gemm_f32_ex(int64_t M, int64_t N, int64_t K, const float *A, int6
     for (int i = 0; i < 2; ++i) {
         const Operand &o = *ops[i];
         if ((reinterpret_cast<uintptr_t>(o.p) & 15) == 0 && (o.ld & 3) == 0) continue;
+        if (gate) return LPY_ERR_NOT_SUPPORTED;   // the repack would read the operand before it arrives
         ld2[i] = (o.inner() + 3) & ~int64_t(3);
         off[i] = scratch_floats;
         scratch_floats += size_t(o.lines() * ld2[i]);
@@ -342,7 +355,19 @@ lpy_status lpy_gemm_f32_ex(int64_t M, int64_t N, int64_t K, const float *A, int6
 
     lpy::Problem prob{int(M), int(N), int(K), oa.p, oa.ld, oa.layout, ob.p, ob.ld, ob.layout, C, ldc};
     lpy::Knobs kn{opts ? opts->num_ctas : 0, opts ? opts->raster_group : 0, opts ? opts->promote_kblocks : 0,
-                  dev.sms, opts ? opts->tile_n : 0};
+                  (opts && opts->plan_sms > 0) ? opts->plan_sms : dev.sms, opts ? opts->tile_n : 0, dev.sms,
+                  lpy::KGate{nullptr, 0, 0, 0, 0}};
+    if (gate) {
+        if ((e = lpy::preload_kgate_signal()) != cudaSuccess) {
+            if (scratch) cudaFreeAsync(scratch, s);
+            return cuda_fail(e);
+        }
+        kn.gate.flags = gate->flags;
+        kn.gate.chunk_k = int(gate->chunk_k);
+        kn.gate.epoch = gate->epoch;
+        kn.gate.timeout_ns = uint64_t(gate->timeout_ms ? gate->timeout_ms : 10000u) * 1000000ull;
+        kn.gate.nchunks = int((K + gate->chunk_k - 1) / gate->chunk_k);
+    }
     if (chosen == LPY_PATH_3XTF32 && !lpy::tf32_supported(prob)) {
         st = (path == LPY_PATH_3XTF32) ? LPY_ERR_NOT_SUPPORTED : LPY_OK;
         if (st == LPY_OK) e = lpy::launch_ffma(prob, kn, s);
@@ -351,6 +376,35 @@ lpy_status lpy_gemm_f32_ex(int64_t M, int64_t N, int64_t K, const float *A, int6
     }
     if (scratch) cudaFreeAsync(scratch, s);
     if (st != LPY_OK) return st;
+    return e == cudaSuccess ? LPY_OK : cuda_fail(e);
+}
+
+}  // namespace
+
+extern "C" {
+
+lpy_status lpy_gemm_f32_ex(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                           lpy_layout layout_a, const float *B, int64_t ldb, lpy_layout layout_b,
+                           float *C, int64_t ldc, lpy_layout layout_c, void *stream, lpy_path path,
+                           const lpy_gemm_opts *opts) {
+    return gemm_impl(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc, layout_c, stream, path, opts, nullptr);
+}
+
+lpy_status lpy_gemm_f32_gated(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                              lpy_layout layout_a, const float *B, int64_t ldb, lpy_layout layout_b,
+                              float *C, int64_t ldc, lpy_layout layout_c, void *stream, lpy_path path,
+                              const lpy_gemm_opts *opts, const lpy_kgate *gate) {
+    if (gate == nullptr) return LPY_ERR_NULL_POINTER;
+    return gemm_impl(M, N, K, A, lda, layout_a, B, ldb, layout_b, C, ldc, layout_c, stream, path, opts, gate);
+}
+
+lpy_status lpy_kgate_signal(uint32_t *flag, uint32_t value, void *stream) {
+    if (flag == nullptr) return LPY_ERR_NULL_POINTER;
+    if (reinterpret_cast<uintptr_t>(flag) & 3) return LPY_ERR_MISALIGNED;
+    DeviceInfo dev;
+    lpy_status st = device_info(dev);
+    if (st != LPY_OK) return st;
+    const cudaError_t e = lpy::launch_kgate_signal(flag, value, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? LPY_OK : cuda_fail(e);
 }
 

@@ -45,12 +45,27 @@ inline cudaError_t ensure_smem_attr(F kern, int bytes, std::atomic<uint64_t> &do
 // the new count.
 int pdl_attr(cudaLaunchAttribute *attrs, int n);
 
+// K-gate of a product whose operands arrive in chunks of K (lpy_kgate in
+// lpy.h; waited on by the kernels' TMA producers, ptx.cuh kgate_wait): no
+// operand element with k in chunk c = [c*chunk_k, (c+1)*chunk_k) is read
+// before flags[c] - epoch >= 0 (wrap-aware).
+struct KGate {
+    const uint32_t *flags;   // nullptr: ungated
+    int chunk_k;             // K indices per flag (>= 32, so a k-block spans <= 2 chunks)
+    uint32_t epoch;
+    uint64_t timeout_ns;     // per wait; exceeded -> __trap() (a deadlock detector)
+    int nchunks;             // ceil(K / chunk_k)
+};
+
 struct Knobs {
     int num_ctas;         // 0 = auto
     int raster_group;     // 0 = auto
     int promote_kblocks;  // 0 = auto
-    int num_sms;          // multiprocessor count of the current device
+    int num_sms;          // SMs the schedule is PLANNED for: opts.plan_sms, else the device's
+                          // (tile width, split-K / stream-K decomposition, default grid)
     int tile_n;           // 0 = auto; else the output-tile width (validated by the front end)
+    int dev_sms;          // multiprocessor count of the current device (co-residency queries)
+    KGate gate;           // flags == nullptr: ungated
 };
 
 // 2-D tensor map over a strided matrix: `inner` contiguous elements per line,
@@ -60,6 +75,9 @@ cudaError_t make_tmap_2d(CUtensorMap *tm, const float *base, uint64_t inner, uin
                          uint64_t ld, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swizzle);
 
 cudaError_t launch_ffma(const Problem &p, const Knobs &k, cudaStream_t s);
+// flag := value (release, GPU scope) once the stream's earlier work is done (kgate.cu)
+cudaError_t launch_kgate_signal(uint32_t *flag, uint32_t value, cudaStream_t s);
+cudaError_t preload_kgate_signal();   // load its module now (lazy loading vs a spinning product)
 // split-K slices for `tiles` output tiles of `k_blocks` k-blocks on `workers`
 // persistent CTAs (pairs); >= min_kb k-blocks per slice, <= max_splits (gemm_ffma.cu)
 int choose_splits(int tiles, int k_blocks, int workers, int min_kb, int max_splits);

@@ -2,8 +2,10 @@
 // tcgen05 (TMEM alloc / mma / commit / ld), fences.  Product code only; the
 // oracle never includes this.
 #pragma once
+#include <climits>
 #include <cstdint>
 #include <cuda.h>
+#include "lpy_internal.h"
 
 namespace lpy {
 
@@ -73,36 +75,6 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, 
         : "memory");
 }
 
-// Non-blocking: 1 if the phase with parity `parity` of `bar` has completed.
-__device__ __forceinline__ uint32_t mbar_test(uint64_t *bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t"
-        ".reg .pred P1;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t"
-        "}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok;
-}
-
-// Wait with cluster-scope acquire (arrivals may come from the peer CTA).
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred P1;\n\t"
-        "LAB_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONE;\n\t"
-        "bra LAB_WAIT;\n\t"
-        "DONE:\n\t"
-        "}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
 // ---------------------------------------------------------------- clusters
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
@@ -143,63 +115,6 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, ui
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
-// Prefetch a 2-D box into L2 (no shared-memory destination, no barrier).
-__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap *tm, int32_t c0, int32_t c1) {
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
-                     reinterpret_cast<uint64_t>(tm)),
-                 "r"(c0), "r"(c1)
-                 : "memory");
-}
-// L2 eviction-priority policies for the .L2::cache_hint loads below.
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ uint64_t l2_policy_evict_last_frac(float f) {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, %1;" : "=l"(p) : "f"(f));
-    return p;
-}
-// Same with an L2 cache-policy hint (createpolicy result).
-__device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *tm, uint64_t *bar,
-                                                 int32_t c0, int32_t c1, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
-        : "memory");
-}
-// 2-D tiled store smem -> global (out-of-bounds parts of the box are clipped).
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap *tm, const void *src, int32_t c0,
-                                             int32_t c1) {
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                     reinterpret_cast<uint64_t>(tm)),
-                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_store_commit() {
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void tma_store_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void tma_store_wait() {
-    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
-}
-
 // ---------------------------------------------------------------- UMMA descriptors
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): start address,
 // leading / stride byte offsets (>> 4), version 1 (sm_100), layout type:
@@ -419,6 +334,58 @@ __device__ __forceinline__ int ld_acquire_gpu(const int *p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+
+// ---------------------------------------------------------------- K-gate (lpy_kgate)
+// A product whose operands arrive in chunks of K (the row-panel product while
+// B is still being broadcast, dist.py): no operand element with k in chunk c
+// is read before flags[c] reaches `epoch` (wrap-aware).  Chunks are published
+// in order, so a producer remembers the highest chunk it has seen ready
+// (`ready`, -1 at the start) and only ever polls the next one.
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Wait until chunks 0..need are ready, then also take every later chunk that
+// is already published (one proxy fence per batch).  The acquire orders this
+// thread's later generic accesses after the publishing release;
+// fence.proxy.async.global then orders its later TMA (async-proxy) reads of
+// global memory after them too.
+__device__ __forceinline__ void kgate_wait(const KGate &g, int &ready, int need) {
+    uint64_t t0 = 0;
+    while (ready < need) {
+        const uint32_t v = ld_acquire_gpu_u32(g.flags + ready + 1);
+        if (int32_t(v - g.epoch) >= 0) {
+            ++ready;
+            continue;
+        }
+        const uint64_t now = globaltimer_ns();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > g.timeout_ns) __trap();
+        __nanosleep(256);
+    }
+    while (ready + 1 < g.nchunks && int32_t(ld_acquire_gpu_u32(g.flags + ready + 1) - g.epoch) >= 0) ++ready;
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// Admit k-block kb (k-blocks of `bk`, K total): wait for the chunks holding it
+// and return the first k-block NOT yet covered by the chunks known ready, so
+// the producer's per-k-block check is one compare (`kb >= limit`) and the
+// slow path runs once per batch of arrived chunks.  (A division per k-block
+// on the producer's critical path cost the 3xTF32 panel 14%: ncu,
+// profiles/r02_gated.txt.)
+__device__ __forceinline__ int kgate_admit(const KGate &g, int &ready, int kb, int bk, int K) {
+    kgate_wait(g, ready, (min(K, (kb + 1) * bk) - 1) / g.chunk_k);
+    if (ready >= g.nchunks - 1) return INT_MAX;
+    return int((int64_t(ready + 1) * g.chunk_k) / bk);
+}
+// Initial admission limit: 0 for a gated product (the first k-block takes the
+// slow path), INT_MAX for an ungated one.
+__device__ __forceinline__ int kgate_limit0(const KGate &g) { return g.flags ? 0 : INT_MAX; }
 
 // Programmatic dependent launch: wait until the grid this one depends on in
 // stream order has completed and its memory is visible (no-op when launched

@@ -1,28 +1,40 @@
-"""Multi-GPU row-panel product (BASELINE.json north_star, SURVEY.md 8(e)).
+"""Multi-GPU row-panel product (BASELINE.json north_star, SURVEY.md 8(b)/8(e)).
 
 C's rows are split into contiguous panels, one per rank (one process per GPU);
 rank r owns rows [r*ceil(M/g), min(M, (r+1)*ceil(M/g))) of A and C
 (reading A14).  Row panels are independent given the whole of B,
 C[rows_r, :] = A[rows_r, :] B, so the only exchange is ONE broadcast of B
-(4*K*N bytes) from the root over NCCL / NVLink; C stays sharded.
+(4*K*N bytes) over NCCL / NVLink; C stays sharded.
 
-To overlap the broadcast with the product, B is held in column-blocked
-storage: `chunks` contiguous blocks, block c a row-major K x w_c matrix
-(the same logical B, different storage -- the paper's layout tags).
-Block c is broadcast on a dedicated communication stream; as soon as it has
-arrived, C[:, cols_c] = A_panel B_c (an lpy_gemm_f32 call writing a disjoint
-column block of C, ldc = N) runs on one of `compute_streams` streams, so the
-product of a block overlaps the broadcast of the next, and the block products
-run concurrently on several streams, each with a persistent grid sized to its
-own tiles (`chunk_grid`), so together they fill the GPU.  Chunk widths are
-multiples of 256 (the 3xTF32 pair tile) so each block is 16-byte aligned.
+The product is fused with its broadcast through the K-gate (include/lpy.h
+lpy_gemm_f32_gated).  Every output tile walks k in order (the reduction
+sum(k, a[i,k]*b[k,j])), so a tile needs the k-th rows of B only
+when it reaches k.  B (row-major K x N) is therefore broadcast in chunks of
+K ROWS -- each one contiguous in memory, so NCCL sends B itself, no re-blocking
+copy -- and after each chunk's broadcast a signal kernel on the communication
+stream publishes flags[c] = epoch.  ONE persistent product over the whole
+panel (the paper's split_iname of the k loop into chunks, whose
+prefetch waits for the chunk) runs at the same time on the caller's
+stream and its TMA producers wait for each chunk's flag before loading it: the
+first tiles start as soon as the first chunk has landed, and the panel is one
+launch with one tile schedule (stream-K balanced over its SM share) instead of
+per-block products that each under-fill the GPU.
 
-The GEMM itself is injected (`gemm_fn`) so the orchestration can be tested
-on CPU with the gloo backend (tests/test_dist.py).
+Scheduling contract: the product spins on flags while it holds its SMs, so it
+is planned for `num_sms - reserve_sms` SMs (opts.plan_sms), leaving the rest to
+NCCL's broadcast kernels and the signal kernel.
+
+Pieces are injectable (`bcast_fn`, `gemm_fn`, `signal_fn`) so the orchestration
+runs on CPU under gloo in the tests (tests/test_dist.py); on CUDA the defaults
+are torch.distributed.broadcast and the library's gated product and signal.
 """
 from __future__ import annotations
 
 import math
+import threading
+
+RESERVE_SMS = 8          # SMs left to the broadcast's NCCL kernels + the signal kernel
+FLAG_WORDS = 4096        # flag array per device (chunks per call <= this)
 
 
 def panel_bounds(M: int, world: int, rank: int) -> tuple[int, int]:
@@ -34,124 +46,320 @@ def panel_bounds(M: int, world: int, rank: int) -> tuple[int, int]:
     return r0, min(M, r0 + h)
 
 
-def chunk_bounds(N: int, chunks: int, align: int = 256) -> list[tuple[int, int]]:
-    """Column blocks [c0, c1) covering [0, N): `chunks` blocks (fewer if N is
-    small) whose widths are multiples of `align` except possibly the last."""
-    if N <= 0:
+def kchunk_bounds(K: int, chunks: int, align: int = 32) -> list[tuple[int, int]]:
+    """K-row ranges [k0, k1) covering [0, K): `chunks` ranges (fewer if K is
+    small) of equal length rounded up to a multiple of `align` (>= 32, the
+    K-gate's minimum), the last one possibly shorter."""
+    if K <= 0:
         return []
-    chunks = max(1, min(chunks, math.ceil(N / align)))
-    w = math.ceil(math.ceil(N / chunks) / align) * align
-    out, c0 = [], 0
-    while c0 < N:
-        out.append((c0, min(N, c0 + w)))
-        c0 += w
+    chunks = max(1, min(chunks, math.ceil(K / align)))
+    w = math.ceil(math.ceil(K / chunks) / align) * align
+    out, k0 = [], 0
+    while k0 < K:
+        out.append((k0, min(K, k0 + w)))
+        k0 += w
     return out
 
 
-def choose_chunks(rows: int, N: int, sms: int = 148, tile: int = 256, max_chunks: int = 8) -> int:
-    """Number of B column blocks for a rank's (rows x N) panel.  The step takes
-    about T_bcast / chunks + T_products(chunks); measured on one B200 at n=8192
-    (scripts/panel_probe.py, profiles/r01_panel_probe.txt) the products lose
-    2-3% at 8 blocks for a 1024-row panel but 8-11% for 2048/4096-row panels,
-    where the broadcast is also a smaller share of the step, so: 8 blocks for
-    panels of <= 1024 rows, 4 up to 2048, else 2 (blocks >= 1024 columns)."""
-    del sms
-    want = 8 if rows <= 1024 else 4 if rows <= 2048 else 2
-    return max(1, min(max_chunks, want, N // (4 * tile)))
+def choose_kchunks(rows: int, K: int, path: str) -> int:
+    """Broadcast chunks of B for a rank's (rows x N) panel: enough that the
+    first chunk (the wait before the first tiles start) is a small share of
+    the step, few enough that NCCL's per-call overhead (~10-20 us) stays
+    hidden.  3xTF32 panels are fast (0.5 ms at 1024 x 8192 x 8192), so 16
+    chunks (512 rows, 16.8 MB at n = 8192); FFMA panels take ~2.3 ms and are
+    insensitive, 8; never chunks shorter than 256 rows of K."""
+    del rows
+    want = 16 if path != "ffma" else 8
+    return max(1, min(want, K // 256))
 
 
-def chunk_streams(rows: int, chunks: int) -> int:
-    """Concurrent compute streams for the block products (same measurement):
-    4 for 1024-row panels, 2 up to 2048, 1 beyond (then one block's product
-    fills the GPU by itself)."""
-    want = 4 if rows <= 1024 else 2 if rows <= 2048 else 1
-    return max(1, min(want, chunks))
-
-
-def chunk_tile_n(path: str) -> int:
-    """Output-tile width (opts.tile_n) for a block product: full-width tiles
-    (256 x 256 per CTA pair on 3xTF32, 128 x 256 per CTA on FFMA) whatever
-    share of the GPU the block's grid gets; the automatic choice would look at
-    the block alone and pick narrower tiles to fill all SMs."""
-    del path
-    return 256
-
-
-def chunk_grid(rows: int, cols: int, sms: int, path: str) -> int:
-    """Persistent grid (CTAs) for one block product sized to its own tiles
-    of width chunk_tile_n (256 x 256 per CTA pair on 3xTF32, 128 x 256 per CTA
-    on FFMA), so concurrent block products share the SMs instead of each
-    claiming all."""
-    tn = chunk_tile_n(path)
-    if path == "3xtf32":
-        return 2 * max(1, min(sms // 2, math.ceil(rows / 256) * math.ceil(cols / tn)))
-    return max(1, min(sms, math.ceil(rows / 128) * math.ceil(cols / tn)))
-
-
-def block_owner(c: int, world: int, root: int = 0, owners: bool = False) -> int:
-    """Rank holding column block c of B before the step: `root` for the
-    north_star's broadcast of B, or rank c mod world when B starts sharded
-    by column blocks (`owners=True`: every rank broadcasts the blocks it holds,
-    so the send load -- and B's generation -- is spread over all ranks; an
-    all-gather of the blocks expressed as per-block broadcasts, since NCCL's
-    all-gather needs equal contiguous pieces and the blocks are column blocks)."""
+def chunk_owner(c: int, world: int, root: int = 0, owners: bool = False) -> int:
+    """Rank holding K-row chunk c of B before the step: `root` (north_star's
+    broadcast of B), or c mod world when B starts sharded by K-row chunks
+    (`owners=True`: every rank broadcasts the chunks it holds -- the send load,
+    and on the host-buffer path the PCIe upload, spread over all ranks)."""
     return c % world if owners else root
 
 
-def rowpanel_gemm(A_panel, B_blocks, C_panel, bounds, group=None, root=0, gemm_fn=None,
-                  comm_stream=None, compute_streams=None, broadcast=True, owners=False):
-    """One distributed product step on this rank.
+def owned_chunks(nchunks: int, world: int, rank: int, root: int = 0, owners: bool = False) -> list[int]:
+    """The K-row chunks of B `rank` holds before the step (and, on the
+    host-buffer path, uploads)."""
+    return [c for c in range(nchunks) if chunk_owner(c, world, root, owners) == rank]
 
-    A_panel : (rows_r, K) tensor, this rank's rows of A.
-    B_blocks: list of (K, w_c) contiguous tensors, the column blocks of B; block
-              c valid on block_owner(c) (root, or c mod world with owners=True),
-              receive buffers elsewhere.  Broadcast in order.
-    C_panel : (rows_r, N) row-major tensor; column block c is written by
-              gemm_fn(A_panel, B_blocks[c], C_panel[:, c0:c1]).
-    bounds  : chunk_bounds(N, len(B_blocks)).
-    On CUDA the caller's current stream is joined to all the work before return
-    (the step is complete in stream order).  Returns the "block arrived" events
-    (CUDA) or None (CPU).
+
+def check_kchunks(bounds, K: int) -> int:
+    """Validate explicit chunk ranges (contiguous from 0 to K, equal lengths
+    >= 32 except a shorter last one) and return the chunk length."""
+    if not bounds:
+        return 32
+    if len(bounds) == 1 and bounds[0] == (0, K):
+        return max(32, K)              # one chunk: all of K (the gate's chunk_k >= 32)
+    w = bounds[0][1] - bounds[0][0]
+    ok = w >= 32 and bounds[0][0] == 0 and bounds[-1][1] == K
+    for i, (k0, k1) in enumerate(bounds):
+        ok = ok and k0 == i * w and (k1 - k0 == w or (i == len(bounds) - 1 and 0 < k1 - k0 <= w))
+    if not ok:
+        raise ValueError(f"bad K chunks {bounds[:4]}... for K={K}")
+    return w
+
+
+class _Flags:
+    """Per-device arrival flags (int32 words, compared as uint32 by the
+    kernels) and the epoch counter: each call raises the epoch, so flags are
+    never reset (lpy_kgate)."""
+
+    def __init__(self, device):
+        import torch
+        self.flags = torch.zeros(FLAG_WORDS, dtype=torch.int32, device=device)
+        self.epoch = 0
+        self.warm = False          # a step has run on this device (its kernels are loaded)
+        self.lock = threading.Lock()
+
+    def next_epoch(self) -> int:
+        with self.lock:
+            self.epoch = (self.epoch + 1) & 0xFFFFFFFF or 1
+            return self.epoch
+
+
+_state: dict = {}
+
+
+def _flags_for(device) -> _Flags:
+    key = ("flags", str(device))
+    if key not in _state:
+        _state[key] = _Flags(device)
+    return _state[key]
+
+
+def _comm_stream(device):
+    import torch
+    key = ("comm", str(device))
+    if key not in _state:
+        _state[key] = torch.cuda.Stream(device=device)
+    return _state[key]
+
+
+def panel_opts(sms: int, reserve_sms: int = RESERVE_SMS):
+    """GemmOpts of the gated panel product: planned for the SMs the broadcast
+    leaves it (results depend on plan_sms, never on the grid)."""
+    from . import GemmOpts
+    o = GemmOpts()
+    o.plan_sms = max(2, sms - reserve_sms)
+    return o
+
+
+def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=None,
+                  reserve_sms=RESERVE_SMS, owners=False, broadcast=True, comm_stream=None,
+                  timings=True, bcast_fn=None, gemm_fn=None, signal_fn=None, before_chunk=None):
+    """One distributed product step on this rank: C_panel = A_panel @ B with B
+    broadcast in K-row chunks while the gated product consumes them.
+
+    A_panel : (rows_r, K) fp32, this rank's rows of A (row- or column-major).
+    B       : (K, N) contiguous row-major fp32; its chunks are valid on their
+              owner (chunk_owner: `root`, or c mod world with owners=True) on
+              entry and on every rank on exit.
+    out     : optional (rows_r, N) fp32 output (row- or column-major).
+    chunks  : number of K-row chunks (None: choose_kchunks) or explicit
+              kchunk_bounds-style [(k0, k1), ...] ranges (each >= 32 rows but
+              the last, equal lengths).
+    before_chunk(c): optional hook run on the communication stream before
+              chunk c's broadcast (the host-buffer step waits for the owner's
+              upload there).
+    Returns (C_panel, info): with timings=True (CUDA) the step is synchronised
+    and info = {"bcast_ms": start -> last chunk broadcast, "gemm_ms": start ->
+    product done, "total_ms": start -> both done, "chunks": n} (the two overlap:
+    gemm_ms includes waiting for chunks); with timings=False info holds the
+    start/bcast/gemm CUDA events instead and nothing is synchronised (the
+    caller's stream is joined to all the work).  On CPU (gloo tests) the chunks
+    are broadcast and signalled in order and then gemm_fn runs.
     """
     import torch
     import torch.distributed as dist
 
-    if gemm_fn is None:
-        from . import gemm as gemm_fn_default
-
-        def gemm_fn(a, b, c):
-            gemm_fn_default(a, b, out=c)
+    if A_panel.dim() != 2 or B.dim() != 2 or A_panel.shape[1] != B.shape[0]:
+        raise ValueError(f"shape mismatch {tuple(A_panel.shape)} @ {tuple(B.shape)}")
+    if not B.is_contiguous():
+        raise ValueError("B must be contiguous row-major: its K-row chunks are broadcast in place")
+    rows, K = A_panel.shape
+    N = B.shape[1]
+    resolved = path
+    if path == "auto" and A_panel.is_cuda:
+        from . import PATH_AUTO, lpy_select_path
+        _, ch = lpy_select_path(rows, N, K, PATH_AUTO)
+        resolved = {1: "ffma", 2: "3xtf32"}[ch]
+    if isinstance(chunks, (list, tuple)):
+        bounds = [tuple(b) for b in chunks]
+    else:
+        bounds = kchunk_bounds(K, chunks or choose_kchunks(rows, K, resolved))
+    chunk_k = check_kchunks(bounds, K)
+    if len(bounds) > FLAG_WORDS:
+        raise ValueError(f"at most {FLAG_WORDS} chunks")
     world = dist.get_world_size(group) if broadcast else 1
-    src = [block_owner(c, world, root, owners) for c in range(len(B_blocks))]
-    if not A_panel.is_cuda:
-        # CPU (gloo) path: same order, no overlap
-        for c, ((c0, c1), blk) in enumerate(zip(bounds, B_blocks)):
-            if broadcast:
-                dist.broadcast(blk, src=src[c], group=group)
-            gemm_fn(A_panel, blk, C_panel[:, c0:c1])
-        return None
+    # a broadcast among one rank moves nothing: skipped (the chunks are still
+    # signalled, so a world-1 step runs the same gated product)
+    broadcast = broadcast and world > 1
+    src = [chunk_owner(c, world, root, owners) for c in range(len(bounds))]
+    if bcast_fn is None:
+        def bcast_fn(t, s):
+            dist.broadcast(t, src=s, group=group)
+    if out is None:
+        out = torch.empty((rows, N), dtype=torch.float32, device=A_panel.device)
 
-    caller = torch.cuda.current_stream()
-    comm = comm_stream or torch.cuda.Stream()
-    streams = compute_streams or [torch.cuda.Stream()
-                                  for _ in range(chunk_streams(A_panel.shape[0], len(B_blocks)))]
-    comm.wait_stream(caller)
-    for st in streams:
-        st.wait_stream(caller)
-    events = []
-    for c, blk in enumerate(B_blocks):
-        if broadcast:
-            with torch.cuda.stream(comm):
-                dist.broadcast(blk, src=src[c], group=group)
-        ev = torch.cuda.Event()
-        ev.record(comm)
-        events.append(ev)
-    for i, ((c0, c1), blk, ev) in enumerate(zip(bounds, B_blocks, events)):
-        st = streams[i % len(streams)]
-        st.wait_event(ev)
-        with torch.cuda.stream(st):
-            gemm_fn(A_panel, blk, C_panel[:, c0:c1])
+    if not A_panel.is_cuda:
+        # CPU (gloo) path: the same sequence without overlap
+        for c, (k0, k1) in enumerate(bounds):
+            if before_chunk is not None:
+                before_chunk(c)
+            if broadcast:
+                bcast_fn(B[k0:k1], src[c])
+            if signal_fn is not None:
+                signal_fn(c, k0, k1)
+        if gemm_fn is None:
+            raise ValueError("CPU tensors need an injected gemm_fn (the product is CUDA-only)")
+        gemm_fn(A_panel, B, out, None)
+        return out, {"chunks": len(bounds)}
+
+    from . import KGate, gemm as lpy_gemm, kgate_signal
+    dev = A_panel.device
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    fl = _flags_for(dev)
+    epoch = fl.next_epoch()
+    caller = torch.cuda.current_stream(dev)
+    comm = comm_stream or _comm_stream(dev)
+    ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "bcast", "gemm")}
+    # fork the communication stream off the caller's work so far -- recorded
+    # BEFORE the product is enqueued, so the chain never waits for the product
+    ev["start"].record(caller)
+    comm.wait_event(ev["start"])
+    gate = KGate(fl.flags.data_ptr(), chunk_k, epoch, 0)
+    opts = panel_opts(sms, reserve_sms)
+
+    def product():
+        if gemm_fn is not None:
+            gemm_fn(A_panel, B, out, (opts, gate))
+        elif K > 0 and rows > 0 and N > 0:
+            lpy_gemm(A_panel, B, out=out, path=path, opts=opts, gate=gate)
+        elif rows > 0 and N > 0:
+            lpy_gemm(A_panel, B, out=out, path=path)      # K == 0: C := 0, nothing to wait for
+        ev["gemm"].record(caller)
+
+    def chain():
+        with torch.cuda.stream(comm):
+            for c, (k0, k1) in enumerate(bounds):
+                if before_chunk is not None:
+                    before_chunk(c)
+                if broadcast:
+                    bcast_fn(B[k0:k1], src[c])
+                if signal_fn is not None:
+                    signal_fn(c, k0, k1)
+                else:
+                    kgate_signal(fl.flags, c, epoch, stream=comm)
+            ev["bcast"].record(comm)
+
+    # Enqueue order.  The first step on a device enqueues the whole chain first:
+    # every kernel it launches (NCCL's, the signal) is then loaded before the
+    # product spins (lazy module loading would otherwise block those first
+    # launches behind it, include/lpy.h).  Later steps enqueue the product
+    # first, so it is running -- its first tiles waiting on chunk 0 -- while
+    # the host is still enqueuing the chain.
+    if fl.warm:
+        product()
+        chain()
+    else:
+        chain()
+        product()
+        fl.warm = True
     caller.wait_stream(comm)
-    for st in streams:
-        caller.wait_stream(st)
-    return events
+    if not timings:
+        return out, {"events": ev, "chunks": len(bounds)}
+    torch.cuda.synchronize(dev)
+    b = ev["start"].elapsed_time(ev["bcast"])
+    g = ev["start"].elapsed_time(ev["gemm"])
+    return out, {"bcast_ms": b, "gemm_ms": g, "total_ms": max(b, g), "chunks": len(bounds)}
+
+
+class HostWorkspace:
+    """Device buffers of the host-buffer step, kept across calls (a serving
+    loop re-uses them; the caching allocator would too, but emulation needs
+    B's non-owned chunks to persist)."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, name, shape, device):
+        import torch
+        t = self.bufs.get(name)
+        if t is None or tuple(t.shape) != tuple(shape) or t.device != device:
+            t = torch.empty(shape, dtype=torch.float32, device=device)
+            self.bufs[name] = t
+        return t
+
+
+def gemm_rowpanel_host(A_panel, B, C_panel, group=None, root=0, chunks=None, path="auto", owners=True,
+                       reserve_sms=RESERVE_SMS, workspace=None, emulate_world=None, broadcast=True):
+    """End-to-end step from HOST buffers (pinned CPU tensors): the multi-GPU
+    counterpart of lpy_gemm_f32_host.  Each rank uploads its A panel and only
+    the K-row chunks of B it owns (chunk_owner: c mod world with owners=True,
+    so each rank moves ~1/g of B over PCIe instead of all of it), the chunks
+    are broadcast over NCCL / NVLink as they land while the gated product
+    consumes them, and the C panel is downloaded into `C_panel`.  Synchronises
+    before returning.  Returns {"h2d_bytes", "d2h_bytes", "chunks"} (this
+    rank's PCIe traffic).
+
+    emulate_world (diagnostics at world 1 only): plan ownership as if there
+    were that many ranks -- rank 0 uploads only its own chunks and the others
+    are taken as already delivered (the workspace must hold them from an
+    earlier call with emulate_world=None); the broadcast is a no-op.
+    """
+    import torch
+    import torch.distributed as dist
+
+    rows, K = A_panel.shape
+    N = B.shape[1]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ws = workspace or _state.setdefault(("host_ws", str(dev)), HostWorkspace())
+    world = dist.get_world_size(group) if broadcast else 1
+    rank = dist.get_rank(group) if broadcast else 0
+    plan_world = emulate_world if (emulate_world and world == 1) else world
+    resolved = path
+    if path == "auto":
+        from . import PATH_AUTO, lpy_select_path
+        _, ch = lpy_select_path(rows, N, K, PATH_AUTO)
+        resolved = {1: "ffma", 2: "3xtf32"}[ch]
+    if isinstance(chunks, (list, tuple)):
+        bounds = [tuple(b) for b in chunks]
+    else:
+        bounds = kchunk_bounds(K, chunks or choose_kchunks(rows, K, resolved))
+    check_kchunks(bounds, K)
+    mine = set(owned_chunks(len(bounds), plan_world, rank, root, owners))
+    dA = ws.get("A", (rows, K), dev)
+    dB = ws.get("B", (K, N), dev)
+    dC = ws.get("C", (rows, N), dev)
+    caller = torch.cuda.current_stream(dev)
+    key = ("h2d", str(dev))
+    if key not in _state:
+        _state[key] = torch.cuda.Stream(device=dev)
+    h2d = _state[key]
+    comm = _comm_stream(dev)
+    h2d.wait_stream(caller)
+    ev_a = torch.cuda.Event()
+    ev_b = [torch.cuda.Event() for _ in bounds]
+    h2d_bytes = 0
+    with torch.cuda.stream(h2d):
+        # A first: the product needs all of its k range from the first chunk on
+        dA.copy_(A_panel, non_blocking=True)
+        h2d_bytes += 4 * rows * K
+        ev_a.record(h2d)
+        for c, (k0, k1) in enumerate(bounds):
+            if c in mine:
+                dB[k0:k1].copy_(B[k0:k1], non_blocking=True)
+                h2d_bytes += 4 * (k1 - k0) * N
+            ev_b[c].record(h2d)
+
+    caller.wait_event(ev_a)
+    gemm_rowpanel(dA, dB, group=group, root=root, chunks=bounds, path=path, out=dC,
+                  reserve_sms=reserve_sms, owners=owners, broadcast=world > 1, comm_stream=comm,
+                  timings=False, before_chunk=lambda c: comm.wait_event(ev_b[c]))
+    C_panel.copy_(dC, non_blocking=True)
+    caller.synchronize()
+    return {"h2d_bytes": h2d_bytes, "d2h_bytes": 4 * rows * N, "chunks": len(bounds)}

@@ -4,7 +4,7 @@ device-resident inputs, 3 warm-up calls, CUDA events around `reps`
 back-to-back calls, median of 3 rounds).  Environment switches of the library
 (e.g. LPY_TF32_STREAMK=0) apply, so A/B runs are two invocations.
 
-usage: python scripts/shapes_time.py <path> M,N,K [M,N,K ...]"""
+usage: [PLAN_SMS=n] python scripts/shapes_time.py <path> M,N,K [M,N,K ...]"""
 import os
 import statistics
 import sys
@@ -17,6 +17,10 @@ import paper_1405_7470_b200 as lpy  # noqa: E402
 
 path = sys.argv[1]
 tag = os.environ.get("TAG", "")
+opts = None
+if os.environ.get("PLAN_SMS"):          # plan for fewer SMs (the row-panel product beside its broadcast)
+    opts = lpy.GemmOpts()
+    opts.plan_sms = int(os.environ["PLAN_SMS"])
 for spec in sys.argv[2:]:
     M, N, K = (int(x) for x in spec.split(","))
     A = torch.rand(M, K, device="cuda") * 2 - 1
@@ -24,14 +28,14 @@ for spec in sys.argv[2:]:
     C = torch.empty(M, N, device="cuda")
     reps = max(3, min(50, int(2e12 / (2.0 * M * N * K) * 10)))
     for _ in range(3):
-        lpy.gemm(A, B, out=C, path=path)
+        lpy.gemm(A, B, out=C, path=path, opts=opts)
     torch.cuda.synchronize()
     res = []
     for _ in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(reps):
-            lpy.gemm(A, B, out=C, path=path)
+            lpy.gemm(A, B, out=C, path=path, opts=opts)
         e1.record()
         torch.cuda.synchronize()
         res.append(e0.elapsed_time(e1) / reps)

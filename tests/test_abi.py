@@ -29,7 +29,8 @@ def test_header_declares_the_boundary():
     assert declared_functions() == sorted([
         "lpy_gemm_f32", "lpy_gemm_f32_ex", "lpy_gemm_f32_host", "lpy_select_path",
         "lpy_status_string", "lpy_last_cuda_error", "lpy_version", "lpy_saxpy_f32",
-        "lpy_saxpy_f32_host", "lpy_coulomb_f32", "lpy_coulomb_f32_host"])
+        "lpy_saxpy_f32_host", "lpy_coulomb_f32", "lpy_coulomb_f32_host", "lpy_gemm_f32_gated",
+        "lpy_kgate_signal"])
 
 
 def test_library_exports_every_declared_symbol():
@@ -40,7 +41,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_version_and_status_strings():
-    assert lpy.lpy_version() == 4
+    assert lpy.lpy_version() == 5
     for code in range(10):
         s = lpy.lpy_status_string(code)
         assert s.startswith("LPY_")
@@ -99,6 +100,38 @@ def test_bad_opts_rejected():
     import torch
     if not torch.cuda.is_available():
         assert call(opts=o) in (6, 8)
+
+
+def test_plan_sms_field_replaces_a_reserved_word():
+    import ctypes as ct
+    assert ct.sizeof(lpy.GemmOpts) == 32          # layout unchanged since version 4
+    assert lpy.GemmOpts.plan_sms.offset == 16
+    o = lpy.GemmOpts()
+    o.plan_sms = -1
+    assert call(opts=o) == 1
+
+
+def gated_call(gate, **kw):
+    args = dict(M=4, N=4, K=64, A=FAKE, lda=64, la=0, B=FAKE + (1 << 20), ldb=4, lb=0,
+                C=FAKE + (2 << 20), ldc=4, lc=0)
+    args.update(kw)
+    return lpy.lpy_gemm_f32_gated(args["M"], args["N"], args["K"], args["A"], args["lda"], args["la"],
+                                  args["B"], args["ldb"], args["lb"], args["C"], args["ldc"], args["lc"],
+                                  None, 0, None, gate)
+
+
+def test_gated_validation_precedes_cuda():
+    flags = FAKE + (3 << 20)
+    assert gated_call(None) == 3                                        # the gate is mandatory
+    assert gated_call(lpy.KGate(0, 32, 1, 0)) == 3                      # NULL flags
+    assert gated_call(lpy.KGate(flags + 2, 32, 1, 0)) == 4              # misaligned flags
+    assert gated_call(lpy.KGate(flags, 16, 1, 0)) == 1                  # chunk_k below 32
+    assert gated_call(lpy.KGate(flags, 1 << 31, 1, 0)) == 1             # chunk_k beyond the dims bound
+    assert gated_call(lpy.KGate(flags, 32, 1, 0), M=-1) == 1            # the operand checks still apply
+    assert gated_call(lpy.KGate(flags, 32, 1, 0), C=FAKE + 8) == 5
+    assert gated_call(lpy.KGate(flags, 32, 1, 0), M=0, A=0, C=0) == 0   # empty domain: no-op
+    assert lpy.lpy_kgate_signal(0, 1, None) == 3
+    assert lpy.lpy_kgate_signal(flags + 1, 1, None) == 4
 
 
 def test_empty_domain_is_noop_without_cuda():

@@ -1,9 +1,10 @@
 """Multi-GPU row-panel orchestration (paper_1405_7470_b200/dist.py) exercised on
-CPU with the gloo backend, world_size 2 and 3: panel/chunk arithmetic, the
-chunked broadcast of B from rank 0, per-block products written into disjoint
-column blocks of C, and concatenated panels equal to the full product.  The
-per-block product is the float64 oracle (test infrastructure) -- the CUDA
-kernels are covered by the GPU tests; here only the host-side logic is."""
+CPU with the gloo backend, world_size 2 and 3: panel / K-chunk arithmetic, the
+chunked broadcast of B's K-row chunks from their owners, the per-chunk arrival
+signal issued after each chunk's broadcast and in chunk order, and concatenated
+panels equal to the full product.  The product itself is the float64 oracle
+(test infrastructure) -- the CUDA kernels and the gated product are covered by
+the GPU tests (tests/test_gated_gpu.py); here only the host-side logic is."""
 import os
 import socket
 
@@ -13,8 +14,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1405_7470_b200.dist import (block_owner, chunk_bounds, chunk_grid, chunk_streams, choose_chunks,
-                                       panel_bounds, rowpanel_gemm)
+from paper_1405_7470_b200.dist import (check_kchunks, choose_kchunks, chunk_owner, gemm_rowpanel, kchunk_bounds,
+                                       owned_chunks, panel_bounds, panel_opts)
 
 
 def test_panel_bounds_cover_rows_exactly():
@@ -29,28 +30,37 @@ def test_panel_bounds_cover_rows_exactly():
         panel_bounds(10, 2, 2)
 
 
-def test_chunk_bounds_aligned_and_covering():
-    for N in (1, 127, 128, 1000, 3000, 8192):
-        for c in (1, 2, 3, 4, 8, 64):
-            b = chunk_bounds(N, c)
-            assert b[0][0] == 0 and b[-1][1] == N
+def test_kchunk_bounds_cover_k_with_equal_chunks():
+    for K in (1, 31, 32, 33, 777, 1000, 4096, 8192):
+        for c in (1, 2, 3, 4, 8, 16, 64):
+            b = kchunk_bounds(K, c)
+            assert b[0][0] == 0 and b[-1][1] == K
             assert all(x1 == y0 for (_, x1), (y0, _) in zip(b, b[1:]))
-            assert all(c0 % 128 == 0 for c0, _ in b)
             assert len(b) <= max(1, c)
-    assert chunk_bounds(8192, 4) == [(0, 2048), (2048, 4096), (4096, 6144), (6144, 8192)]
-    assert chunk_bounds(0, 4) == []
+            w = check_kchunks(b, K)                     # equal widths, >= 32, multiple of 32
+            assert w >= 32 and (len(b) == 1 or w % 32 == 0)
+    assert kchunk_bounds(8192, 16)[1] == (512, 1024)
+    assert kchunk_bounds(0, 4) == []
+    with pytest.raises(ValueError):
+        check_kchunks([(0, 16), (16, 32)], 32)         # below the gate's 32-row minimum
+    with pytest.raises(ValueError):
+        check_kchunks([(0, 64), (64, 96), (96, 192)], 192)   # unequal widths
 
 
-def test_chunk_policy():
-    # n = 8192 panels for g = 8 / 4 / 2 / 1 ranks
-    assert [choose_chunks(8192 // g, 8192) for g in (8, 4, 2, 1)] == [8, 4, 2, 2]
-    assert [chunk_streams(8192 // g, choose_chunks(8192 // g, 8192)) for g in (8, 4, 2, 1)] == [4, 2, 1, 1]
-    assert choose_chunks(1024, 1000) == 1 and choose_chunks(1024, 0) == 1
-    # grids sized to a block's own tiles, never beyond the chip
-    assert chunk_grid(1024, 1024, 148, "3xtf32") == 32      # 16 pair tiles
-    assert chunk_grid(8192, 8192, 148, "3xtf32") == 148
-    assert chunk_grid(1024, 1024, 148, "ffma") == 32
-    assert chunk_grid(1, 1, 148, "ffma") == 1
+def test_chunk_policy_and_ownership():
+    assert choose_kchunks(1024, 8192, "3xtf32") == 16
+    assert choose_kchunks(1024, 8192, "ffma") == 8
+    assert choose_kchunks(1024, 300, "3xtf32") == 1
+    assert [chunk_owner(c, 4) for c in range(6)] == [0] * 6
+    assert [chunk_owner(c, 4, owners=True) for c in range(6)] == [0, 1, 2, 3, 0, 1]
+    # every chunk has exactly one owner; owners spread them evenly
+    for g in (1, 2, 3, 8):
+        for owners in (False, True):
+            got = sorted(c for r in range(g) for c in owned_chunks(16, g, r, 0, owners))
+            assert got == list(range(16))
+    assert owned_chunks(16, 8, 0, owners=True) == [0, 8]       # 1/8 of B per rank
+    o = panel_opts(148)
+    assert o.plan_sms == 140 and o.num_ctas == 0 and list(o.reserved) == [0, 0, 0]
 
 
 def _free_port():
@@ -70,29 +80,28 @@ def _worker(rank, world, port, M, N, K, chunks, q, owners=False):
     try:
         r0, r1 = panel_bounds(M, world, rank)
         A = torch.from_numpy(synth.matrix(r1 - r0, K, seed=3, matrix_id=0, row0=r0))
-        bounds = chunk_bounds(N, chunks)
-        blocks = []
-        for c, (c0, c1) in enumerate(bounds):
-            if rank == block_owner(c, world, 0, owners):
-                blocks.append(torch.from_numpy(synth.matrix(K, c1 - c0, seed=3, matrix_id=1, col0=c0)))
-            else:
-                blocks.append(torch.full((K, c1 - c0), float("nan")))
-        C = torch.full((r1 - r0, N), float("nan"))
+        Bfull = torch.from_numpy(synth.matrix(K, N, seed=3, matrix_id=1))
+        bounds = kchunk_bounds(K, chunks)
+        B = torch.full((K, N), float("nan"))
+        for c in owned_chunks(len(bounds), world, rank, 0, owners):
+            k0, k1 = bounds[c]
+            B[k0:k1] = Bfull[k0:k1]
+        events = []
 
-        def gemm_fn(a, b, c):
+        def signal_fn(c, k0, k1):
+            # the chunk has arrived when its flag is raised
+            events.append((c, bool(torch.isnan(B[k0:k1]).any())))
+
+        def gemm_fn(a, b, c, _gate):
             m, k = a.shape
             n = b.shape[1]
             ref, _ = oracle.gemm(m, n, k, a.contiguous().numpy().reshape(-1), k, 0,
                                  b.contiguous().numpy().reshape(-1), n, 0)
             c.copy_(torch.from_numpy(ref.astype(np.float32)))
 
-        rowpanel_gemm(A, blocks, C, bounds, gemm_fn=gemm_fn, owners=owners)
-        # every rank now holds all of B (the broadcast), and its panel of C
-        B_full = torch.cat(blocks, dim=1)
-        if rank == 0:
-            q.put(("ok", B_full.numpy(), None, C.numpy()))
-        else:
-            q.put(("ok_rank", rank, bool(torch.isnan(B_full).any()), C.numpy()))
+        C, info = gemm_rowpanel(A, B, chunks=chunks, owners=owners, gemm_fn=gemm_fn, signal_fn=signal_fn)
+        assert info["chunks"] == len(bounds)
+        q.put(("ok", rank, bool(torch.equal(B, Bfull)), events, C.numpy()))
     except Exception as e:   # surface worker failures to the parent
         q.put(("err", repr(e)))
         raise
@@ -101,8 +110,8 @@ def _worker(rank, world, port, M, N, K, chunks, q, owners=False):
 
 
 @pytest.mark.parametrize("world,M,N,K,chunks,owners", [(2, 256, 384, 96, 3, False), (3, 200, 300, 64, 2, False),
-                                                       (2, 130, 128, 33, 1, False), (3, 256, 768, 40, 3, True),
-                                                       (2, 300, 1024, 24, 4, True)])
+                                                       (2, 130, 128, 33, 1, False), (3, 256, 200, 160, 5, True),
+                                                       (2, 300, 100, 130, 4, True)])
 def test_rowpanel_gloo(world, M, N, K, chunks, owners):
     import oracle
     import synth
@@ -121,13 +130,12 @@ def test_rowpanel_gloo(world, M, N, K, chunks, owners):
     A = synth.matrix(M, K, seed=3, matrix_id=0)
     B = synth.matrix(K, N, seed=3, matrix_id=1)
     Cref, _ = oracle.gemm(M, N, K, A.reshape(-1), K, 0, B.reshape(-1), N, 0)
+    nb = len(kchunk_bounds(K, chunks))
     panels = {}
-    for r in results:
-        if r[0] == "ok":
-            assert np.array_equal(r[1], B)                  # rank 0 kept B intact
-            panels[0] = r[3]
-        else:
-            assert not r[2], "broadcast left NaNs in B on a receiving rank"
-            panels[r[1]] = r[3]
+    for _, rank, b_ok, events, C in results:
+        assert b_ok, f"rank {rank}: B incomplete after the broadcast"
+        assert [c for c, _ in events] == list(range(nb)), "chunks signalled out of order"
+        assert not any(nan for _, nan in events), "a chunk was signalled before it arrived"
+        panels[rank] = C
     C = np.concatenate([panels[r] for r in range(world)], axis=0)
     assert np.array_equal(C, Cref.astype(np.float32))
