@@ -4,6 +4,11 @@
   liblpy_probe.so  hardware probes (tcgen05 numerics, MMA / FFMA rates) for tests
   liblpy_trace.so  diagnostics: the product built with -DLPY_TRACE (per-CTA cycle
                    counters in the 3xTF32 kernel); never loaded by the product path
+  liblpy_mutant.so the product with -DLPY_MUTATE_STAGE_RACE: each kernel's stage
+                   hand-off broken (FFMA consumers release a stage before reading
+                   it, the 3xTF32 MMA skips the wait for its stage) -- the race
+                   detector tests must FAIL on it (tests/test_mutation_gpu.py);
+                   never loaded by the product path
 
 nvcc cross-compiles here without a GPU.  The explicit `-gencode
 arch=compute_100a,code=sm_100a` form is required: plain -arch=sm_100a does not
@@ -27,6 +32,7 @@ BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "liblpy.so")
 PROBE_LIB = os.path.join(PKG, "liblpy_probe.so")
 TRACE_LIB = os.path.join(PKG, "liblpy_trace.so")
+MUTANT_LIB = os.path.join(PKG, "liblpy_mutant.so")
 
 SOURCES = ["lpy_api.cu", "gemm_ffma.cu", "gemm_3xtf32.cu", "repack.cu", "saxpy.cu", "coulomb.cu", "kgate.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -37,11 +43,14 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"
 OBJECTS = [(os.path.splitext(s)[0], s, []) for s in SOURCES] + [
     ("probe_tcgen05", "probe_tcgen05.cu", []),
     ("gemm_3xtf32_trace", "gemm_3xtf32.cu", ["-DLPY_TRACE"]),
+    ("gemm_ffma_mutant", "gemm_ffma.cu", ["-DLPY_MUTATE_STAGE_RACE"]),
+    ("gemm_3xtf32_mutant", "gemm_3xtf32.cu", ["-DLPY_MUTATE_STAGE_RACE"]),
 ]
 LIBS = [
     (LIB, [os.path.splitext(s)[0] for s in SOURCES]),
     (PROBE_LIB, ["probe_tcgen05"]),
     (TRACE_LIB, ["lpy_api", "gemm_ffma", "gemm_3xtf32_trace", "repack", "saxpy", "coulomb", "kgate"]),
+    (MUTANT_LIB, ["lpy_api", "gemm_ffma_mutant", "gemm_3xtf32_mutant", "repack", "saxpy", "coulomb", "kgate"]),
 ]
 
 

@@ -398,7 +398,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                         tc_fence_after();
                     }
                     TR_T0(t_r);
+#ifndef LPY_MUTATE_STAGE_RACE
                     mbar_wait(&ready[s], ph);
+#endif
+                    // (MUTATION liblpy_mutant.so, tests/test_mutation_gpu.py only: the MMA
+                    // skips the wait for the stage's TMA + split transform)
                     TR_ADD(1, t_r);
                     if (kb == kb0 && u == unit0 && lane == 0) TL(4);
                     if (kb == kb0 && su >= 0 && lane == 0 && su < p.sk_stride) TLC(6);

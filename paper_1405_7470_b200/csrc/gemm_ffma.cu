@@ -291,6 +291,12 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
             if constexpr (G::X) mbar_wait(&xfull[stage], phase);
             const float *sa = G::XA ? x_a(stage) : raw_a(stage);
             const float *sb = G::XB ? x_b(stage) : raw_b(stage);
+#ifdef LPY_MUTATE_STAGE_RACE
+            // MUTATION (liblpy_mutant.so, tests/test_mutation_gpu.py only): the
+            // stage is released BEFORE it is read, so the producer may refill it
+            // under the consumers -- the race the detector tests must catch
+            mbar_arrive_after_reads(&empty[stage], lane);
+#endif
 #pragma unroll
             for (int k = 0; k < BK; ++k) {
                 float a[8], b[2 * JN];
@@ -304,7 +310,9 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
 #pragma unroll
                     for (int jp = 0; jp < JN; ++jp) ffma2(acc2[i][jp], a[i], bp[jp]);
             }
+#ifndef LPY_MUTATE_STAGE_RACE
             mbar_arrive_after_reads(&empty[stage], lane);
+#endif
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
 
