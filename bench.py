@@ -270,15 +270,15 @@ def time_path(args, path, rank, world, device, dist_on):
     import torch
     import paper_1405_7470_b200 as lpy
     from paper_1405_7470_b200.dist import (choose_kchunks, gemm_rowpanel, kchunk_bounds, owned_chunks,
-                                          panel_bounds, panel_opts, chunk_owner)
+                                          panel_bounds, panel_opts, chunk_owner, transfers)
     n = args.n
     pw = args.emulate_ranks if (args.emulate_ranks and world == 1) else world   # panel split
     r0, r1 = panel_bounds(n, pw, rank)
     rows = r1 - r0
     sms = torch.cuda.get_device_properties(device).multi_processor_count
-    owners = args.bcast == "owners"
+    mode = args.bcast
     bounds = kchunk_bounds(n, args.chunks or choose_kchunks(rows, n, path)) if dist_on else [(0, n)]
-    mine = owned_chunks(len(bounds), world, rank, 0, owners) if dist_on else [0]
+    mine = owned_chunks(len(bounds), world, rank, 0, mode) if dist_on else [0]
     Ah, Bh = host_inputs(n, r0, r1, [bounds[c] for c in mine] if dist_on and world > 1 else None)
     A = torch.from_numpy(Ah).to(device)
     B = torch.from_numpy(Bh).to(device)
@@ -289,7 +289,7 @@ def time_path(args, path, rank, world, device, dist_on):
         if not dist_on:
             lpy.gemm(A, B, out=C, path=path)
         else:
-            gemm_rowpanel(A, B, chunks=bounds, path=path, out=C, owners=owners, reserve_sms=args.reserve_sms,
+            gemm_rowpanel(A, B, chunks=bounds, path=path, out=C, bcast=mode, reserve_sms=args.reserve_sms,
                           timings=False)
 
     for _ in range(args.warmup):
@@ -339,8 +339,17 @@ def time_path(args, path, rank, world, device, dist_on):
         # chunked broadcast (4*K*N bytes from the owners) and this rank's
         # product planned for the same SMs, ungated (bitwise the gated one)
         opts = panel_opts(sms, args.reserve_sms)
-        bcast_ms = timed(lambda: [dist.broadcast(B[k0:k1], src=chunk_owner(c, world, 0, owners))
-                                  for c, (k0, k1) in enumerate(bounds)], reps)
+        plan = transfers(bounds, world, 0, mode)
+
+        def comm_only():
+            for kind, cs in plan:
+                if kind == "bcast":
+                    k0, k1 = bounds[cs[0]]
+                    dist.broadcast(B[k0:k1], src=chunk_owner(cs[0], world, 0, mode))
+                else:
+                    p0, p1 = bounds[cs[rank]]
+                    dist.all_gather_into_tensor(B[bounds[cs[0]][0]:bounds[cs[-1]][1]], B[p0:p1])
+        bcast_ms = timed(comm_only, reps)
         gemm_ms = timed(lambda: lpy.gemm(A, B, out=C, path=path, opts=opts), reps)
         nbytes = 4 * n * n
         multi = {"total_ms": round(total_ms / args.steps, 4), "bcast_ms": round(bcast_ms, 4),
@@ -425,10 +434,11 @@ def time_e2e(args, path, rank, world, device, dist_on):
             return 4 * (rows * n + n * n), 4 * rows * n
     else:
         # host buffers: every rank uploads only the K-row chunks it owns (c mod
-        # N), so B crosses PCIe once in total, then NVLink (owners broadcast)
-        owners = True
+        # N), so B crosses PCIe once in total, then NVLink (owners broadcast, or
+        # the all-gather rounds with --bcast allgather)
+        mode = "allgather" if args.bcast == "allgather" else "owners"
         bounds = kchunk_bounds(n, args.chunks or choose_kchunks(rows, n, path))
-        mine = owned_chunks(len(bounds), pw, rank, 0, owners)
+        mine = owned_chunks(len(bounds), pw, rank, 0, mode)
         _, Bh = host_inputs(n, r0, r1, [bounds[c] for c in mine] if (world > 1 or emul) else None)
         B = torch.from_numpy(Bh).pin_memory()
         del Bh
@@ -442,7 +452,7 @@ def time_e2e(args, path, rank, world, device, dist_on):
             del Bfull
 
         def step():
-            info = gemm_rowpanel_host(A, B, C, chunks=bounds, path=path, owners=owners,
+            info = gemm_rowpanel_host(A, B, C, chunks=bounds, path=path, bcast=mode,
                                       reserve_sms=args.reserve_sms, workspace=ws, emulate_world=emul)
             return info["h2d_bytes"], info["d2h_bytes"]
 
@@ -634,9 +644,12 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "ffma", "3xtf32"])
     ap.add_argument("--also", default="ffma", help="secondary path to report ('' for none)")
     ap.add_argument("--chunks", type=int, default=0, help="K-row chunks of B for N>1 (0 = dist.choose_kchunks)")
-    ap.add_argument("--bcast", default="root", choices=["root", "owners"],
+    ap.add_argument("--bcast", default="root", choices=["root", "owners", "allgather"],
                     help="N>1: B starts on rank 0 and is broadcast (north_star), or starts sharded by "
-                         "K-row chunks (chunk c on rank c mod N) and each owner broadcasts its chunks")
+                         "K-row chunks (chunk c on rank c mod N) and each owner broadcasts its chunks, or "
+                         "rounds of N chunks are all-gathered (NCCL may run them as NVLS: --nccl-algo)")
+    ap.add_argument("--nccl-algo", default="",
+                    help="N>1: NCCL_ALGO for the run (e.g. NVLS, Ring); default: NCCL's own choice")
     ap.add_argument("--reserve-sms", type=int, default=8,
                     help="N>1: SMs the gated product leaves to the broadcast (dist.RESERVE_SMS)")
     ap.add_argument("--emulate-ranks", type=int, default=0,
@@ -679,6 +692,11 @@ def main():
             os.environ.setdefault("WORLD_SIZE", "1")
         # NCCL's INIT lines (rank / nRanks / transport per communicator) go to stderr,
         # where the launcher's rank check reads them
+        if args.nccl_algo:
+            os.environ["NCCL_ALGO"] = args.nccl_algo
+        # the gated product leaves --reserve-sms SMs to the collective: NCCL may not
+        # launch more CTAs than that (more would queue behind the product's grid)
+        os.environ.setdefault("NCCL_MAX_CTAS", str(max(1, args.reserve_sms)))
         if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
             os.environ["NCCL_DEBUG"] = "INFO"
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
@@ -744,7 +762,7 @@ def main():
             "data": "synthetic: seeded SplitMix64 uniform[-1,1) fp32 on a 2^-23 grid",
             "config": {"workload": f"n={n} square fp32 C=A*B, row-major A/B/C (BASELINE config 4)",
                        "path": res["path"], "M": n, "N": n, "K": n,
-                       "parallelism": f"rowpanel{world}" + (f"+nccl_bcast_B_kchunks{res['chunks']}" + ("_owners" if args.bcast == "owners" else "") + "+gated_product" if dist_on else ""),
+                       "parallelism": f"rowpanel{world}" + (f"+nccl_{args.bcast}_B_kchunks{res['chunks']}" + "+gated_product" if dist_on else ""),
                        "l2": "inputs larger than L2 (A, B, C 268 MB each > 126 MB), no flush"},
             "roofline": roof(res, res["path"]),
             "cpu_baseline": cpu,

@@ -6,7 +6,8 @@
                    counters in the 3xTF32 kernel); never loaded by the product path
   liblpy_mutant.so the product with -DLPY_MUTATE_STAGE_RACE: each kernel's stage
                    hand-off broken (FFMA consumers release a stage before reading
-                   it, the 3xTF32 MMA skips the wait for its stage) -- the race
+                   it, the 3xTF32 split transform marks a stage ready before
+                   writing its small parts) -- the race
                    detector tests must FAIL on it (tests/test_mutation_gpu.py);
                    never loaded by the product path
 

@@ -398,11 +398,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         tc_fence_after();
                     }
                     TR_T0(t_r);
-#ifndef LPY_MUTATE_STAGE_RACE
                     mbar_wait(&ready[s], ph);
-#endif
-                    // (MUTATION liblpy_mutant.so, tests/test_mutation_gpu.py only: the MMA
-                    // skips the wait for the stage's TMA + split transform)
                     TR_ADD(1, t_r);
                     if (kb == kb0 && u == unit0 && lane == 0) TL(4);
                     if (kb == kb0 && su >= 0 && lane == 0 && su < p.sk_stride) TLC(6);
@@ -459,6 +455,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                 TR_ADD(4, t_f);
                 if (kb == kb0 && u == unit0 && xt == 0) TL(3);
                 TR_T0(t_x);
+#ifdef LPY_MUTATE_STAGE_RACE
+                // MUTATION (liblpy_mutant.so, tests/test_mutation_gpu.py only): the
+                // stage is declared ready BEFORE its small parts are written, so the
+                // MMA may read stale ones -- the race the detector tests must catch
+                if (lane == 0) arrive_leader<CG>(&ready[s], lead);
+#endif
                 const float4 *src = reinterpret_cast<const float4 *>(stages + s * STAGE_BYTES);
                 float4 *dst = reinterpret_cast<float4 *>(stages + s * STAGE_BYTES + RAW_BYTES);
 #pragma unroll 4
@@ -472,7 +474,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
+#ifndef LPY_MUTATE_STAGE_RACE
                 if (lane == 0) arrive_leader<CG>(&ready[s], lead);
+#endif
                 if (++s == STAGES) { s = 0; ph ^= 1; }
                 TR_ADD(6, t_x);
             }

@@ -73,18 +73,51 @@ def choose_kchunks(rows: int, K: int, path: str) -> int:
     return max(1, min(want, K // 256))
 
 
-def chunk_owner(c: int, world: int, root: int = 0, owners: bool = False) -> int:
-    """Rank holding K-row chunk c of B before the step: `root` (north_star's
-    broadcast of B), or c mod world when B starts sharded by K-row chunks
-    (`owners=True`: every rank broadcasts the chunks it holds -- the send load,
-    and on the host-buffer path the PCIe upload, spread over all ranks)."""
-    return c % world if owners else root
+BCAST_MODES = ("root", "owners", "allgather")
 
 
-def owned_chunks(nchunks: int, world: int, rank: int, root: int = 0, owners: bool = False) -> list[int]:
+def chunk_owner(c: int, world: int, root: int = 0, mode: str = "root") -> int:
+    """Rank holding K-row chunk c of B before the step: `root` in mode "root"
+    (north_star's broadcast of B), else c mod world -- B starts sharded by
+    K-row chunks and every rank sends the chunks it holds ("owners": one NCCL
+    broadcast per chunk from its owner; "allgather": one NCCL all-gather per
+    round of `world` consecutive chunks, SURVEY 8(f)-3's all-gather from
+    pre-sharded B, which NCCL can run as NVLS on NVSwitch).  Either way the send
+    load -- and on the host-buffer path the PCIe upload -- is spread over all
+    ranks."""
+    if mode not in BCAST_MODES:
+        raise ValueError(f"bcast mode {mode!r} not in {BCAST_MODES}")
+    return root if mode == "root" else c % world
+
+
+def owned_chunks(nchunks: int, world: int, rank: int, root: int = 0, mode: str = "root") -> list[int]:
     """The K-row chunks of B `rank` holds before the step (and, on the
     host-buffer path, uploads)."""
-    return [c for c in range(nchunks) if chunk_owner(c, world, root, owners) == rank]
+    return [c for c in range(nchunks) if chunk_owner(c, world, root, mode) == rank]
+
+
+def transfers(bounds, world: int, root: int = 0, mode: str = "root") -> list[tuple[str, list[int]]]:
+    """The communication plan of one step: ("bcast", [c]) broadcasts chunk c
+    from its owner; ("allgather", [c0 .. c0+world-1]) all-gathers a round of
+    `world` consecutive equal chunks, chunk c0+r coming from rank r, in place
+    (the round's rows of B are contiguous and rank r's piece sits at offset r
+    in them, as NCCL's in-place all-gather wants).  A round that would be
+    partial, or hold a shorter last chunk, falls back to per-chunk broadcasts.
+    Chunks are delivered in increasing order (the gate polls them in order)."""
+    n = len(bounds)
+    if mode != "allgather" or world == 1:
+        return [("bcast", [c]) for c in range(n)]
+    w = bounds[0][1] - bounds[0][0] if bounds else 0
+    plan, c = [], 0
+    while c < n:
+        rnd = list(range(c, c + world))
+        if rnd[-1] < n and all(bounds[x][1] - bounds[x][0] == w for x in rnd):
+            plan.append(("allgather", rnd))
+            c += world
+        else:
+            plan.append(("bcast", [c]))
+            c += 1
+    return plan
 
 
 def check_kchunks(bounds, K: int) -> int:
@@ -149,15 +182,17 @@ def panel_opts(sms: int, reserve_sms: int = RESERVE_SMS):
 
 
 def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=None,
-                  reserve_sms=RESERVE_SMS, owners=False, broadcast=True, comm_stream=None,
-                  timings=True, bcast_fn=None, gemm_fn=None, signal_fn=None, before_chunk=None):
+                  reserve_sms=RESERVE_SMS, bcast="root", broadcast=True, comm_stream=None,
+                  timings=True, bcast_fn=None, gather_fn=None, gemm_fn=None, signal_fn=None,
+                  before_chunk=None):
     """One distributed product step on this rank: C_panel = A_panel @ B with B
     broadcast in K-row chunks while the gated product consumes them.
 
     A_panel : (rows_r, K) fp32, this rank's rows of A (row- or column-major).
     B       : (K, N) contiguous row-major fp32; its chunks are valid on their
-              owner (chunk_owner: `root`, or c mod world with owners=True) on
-              entry and on every rank on exit.
+              owner (chunk_owner: `root` with bcast="root", else c mod world)
+              on entry and on every rank on exit.
+    bcast   : "root" | "owners" | "allgather" (chunk_owner, transfers).
     out     : optional (rows_r, N) fp32 output (row- or column-major).
     chunks  : number of K-row chunks (None: choose_kchunks) or explicit
               kchunk_bounds-style [(k0, k1), ...] ranges (each >= 32 rows but
@@ -198,22 +233,36 @@ def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=
     # a broadcast among one rank moves nothing: skipped (the chunks are still
     # signalled, so a world-1 step runs the same gated product)
     broadcast = broadcast and world > 1
-    src = [chunk_owner(c, world, root, owners) for c in range(len(bounds))]
+    src = [chunk_owner(c, world, root, bcast) for c in range(len(bounds))]
+    plan = transfers(bounds, world, root, bcast)
     if bcast_fn is None:
         def bcast_fn(t, s):
             dist.broadcast(t, src=s, group=group)
+    if gather_fn is None:
+        def gather_fn(out_rows, piece):
+            dist.all_gather_into_tensor(out_rows, piece, group=group)
+    rank = dist.get_rank(group) if broadcast else 0
+
+    def run_plan(signal):
+        for kind, cs in plan:
+            if before_chunk is not None:
+                for c in cs:
+                    before_chunk(c)
+            if broadcast and kind == "bcast":
+                k0, k1 = bounds[cs[0]]
+                bcast_fn(B[k0:k1], src[cs[0]])
+            elif broadcast:
+                k0, k1 = bounds[cs[0]][0], bounds[cs[-1]][1]
+                p0, p1 = bounds[cs[rank]]
+                gather_fn(B[k0:k1], B[p0:p1])
+            for c in cs:
+                signal(c)
     if out is None:
         out = torch.empty((rows, N), dtype=torch.float32, device=A_panel.device)
 
     if not A_panel.is_cuda:
         # CPU (gloo) path: the same sequence without overlap
-        for c, (k0, k1) in enumerate(bounds):
-            if before_chunk is not None:
-                before_chunk(c)
-            if broadcast:
-                bcast_fn(B[k0:k1], src[c])
-            if signal_fn is not None:
-                signal_fn(c, k0, k1)
+        run_plan(lambda c: signal_fn(c, *bounds[c]) if signal_fn is not None else None)
         if gemm_fn is None:
             raise ValueError("CPU tensors need an injected gemm_fn (the product is CUDA-only)")
         gemm_fn(A_panel, B, out, None)
@@ -245,15 +294,8 @@ def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=
 
     def chain():
         with torch.cuda.stream(comm):
-            for c, (k0, k1) in enumerate(bounds):
-                if before_chunk is not None:
-                    before_chunk(c)
-                if broadcast:
-                    bcast_fn(B[k0:k1], src[c])
-                if signal_fn is not None:
-                    signal_fn(c, k0, k1)
-                else:
-                    kgate_signal(fl.flags, c, epoch, stream=comm)
+            run_plan(lambda c: signal_fn(c, *bounds[c]) if signal_fn is not None
+                     else kgate_signal(fl.flags, c, epoch, stream=comm))
             ev["bcast"].record(comm)
 
     # Enqueue order.  The first step on a device enqueues the whole chain first:
@@ -295,12 +337,13 @@ class HostWorkspace:
         return t
 
 
-def gemm_rowpanel_host(A_panel, B, C_panel, group=None, root=0, chunks=None, path="auto", owners=True,
+def gemm_rowpanel_host(A_panel, B, C_panel, group=None, root=0, chunks=None, path="auto", bcast="owners",
                        reserve_sms=RESERVE_SMS, workspace=None, emulate_world=None, broadcast=True):
     """End-to-end step from HOST buffers (pinned CPU tensors): the multi-GPU
     counterpart of lpy_gemm_f32_host.  Each rank uploads its A panel and only
-    the K-row chunks of B it owns (chunk_owner: c mod world with owners=True,
-    so each rank moves ~1/g of B over PCIe instead of all of it), the chunks
+    the K-row chunks of B it owns (chunk_owner: c mod world with bcast
+    "owners" or "allgather", so each rank moves ~1/g of B over PCIe instead of
+    all of it), the chunks
     are broadcast over NCCL / NVLink as they land while the gated product
     consumes them, and the C panel is downloaded into `C_panel`.  Synchronises
     before returning.  Returns {"h2d_bytes", "d2h_bytes", "chunks"} (this
@@ -331,7 +374,7 @@ def gemm_rowpanel_host(A_panel, B, C_panel, group=None, root=0, chunks=None, pat
     else:
         bounds = kchunk_bounds(K, chunks or choose_kchunks(rows, K, resolved))
     check_kchunks(bounds, K)
-    mine = set(owned_chunks(len(bounds), plan_world, rank, root, owners))
+    mine = set(owned_chunks(len(bounds), plan_world, rank, root, bcast))
     dA = ws.get("A", (rows, K), dev)
     dB = ws.get("B", (K, N), dev)
     dC = ws.get("C", (rows, N), dev)
@@ -358,7 +401,7 @@ def gemm_rowpanel_host(A_panel, B, C_panel, group=None, root=0, chunks=None, pat
 
     caller.wait_event(ev_a)
     gemm_rowpanel(dA, dB, group=group, root=root, chunks=bounds, path=path, out=dC,
-                  reserve_sms=reserve_sms, owners=owners, broadcast=world > 1, comm_stream=comm,
+                  reserve_sms=reserve_sms, bcast=bcast, broadcast=world > 1, comm_stream=comm,
                   timings=False, before_chunk=lambda c: comm.wait_event(ev_b[c]))
     C_panel.copy_(dC, non_blocking=True)
     caller.synchronize()

@@ -15,7 +15,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_1405_7470_b200.dist import (check_kchunks, choose_kchunks, chunk_owner, gemm_rowpanel, kchunk_bounds,
-                                       owned_chunks, panel_bounds, panel_opts)
+                                       owned_chunks, panel_bounds, panel_opts, transfers)
 
 
 def test_panel_bounds_cover_rows_exactly():
@@ -52,13 +52,33 @@ def test_chunk_policy_and_ownership():
     assert choose_kchunks(1024, 8192, "ffma") == 8
     assert choose_kchunks(1024, 300, "3xtf32") == 1
     assert [chunk_owner(c, 4) for c in range(6)] == [0] * 6
-    assert [chunk_owner(c, 4, owners=True) for c in range(6)] == [0, 1, 2, 3, 0, 1]
+    assert [chunk_owner(c, 4, mode="owners") for c in range(6)] == [0, 1, 2, 3, 0, 1]
+    assert [chunk_owner(c, 4, mode="allgather") for c in range(6)] == [0, 1, 2, 3, 0, 1]
+    with pytest.raises(ValueError):
+        chunk_owner(0, 4, mode="nvls")
     # every chunk has exactly one owner; owners spread them evenly
     for g in (1, 2, 3, 8):
-        for owners in (False, True):
-            got = sorted(c for r in range(g) for c in owned_chunks(16, g, r, 0, owners))
+        for mode in ("root", "owners", "allgather"):
+            got = sorted(c for r in range(g) for c in owned_chunks(16, g, r, 0, mode))
             assert got == list(range(16))
-    assert owned_chunks(16, 8, 0, owners=True) == [0, 8]       # 1/8 of B per rank
+    assert owned_chunks(16, 8, 0, mode="owners") == [0, 8]       # 1/8 of B per rank
+
+
+def test_transfer_plan():
+    b16 = kchunk_bounds(8192, 16)
+    assert transfers(b16, 8, mode="root") == [("bcast", [c]) for c in range(16)]
+    assert transfers(b16, 8, mode="allgather") == [("allgather", list(range(8))), ("allgather", list(range(8, 16)))]
+    assert transfers(b16, 1, mode="allgather") == [("bcast", [c]) for c in range(16)]
+    # a partial last round and a short last chunk fall back to broadcasts
+    b5 = kchunk_bounds(160, 5)          # 5 chunks of 32
+    assert transfers(b5, 2, mode="allgather") == [("allgather", [0, 1]), ("allgather", [2, 3]), ("bcast", [4])]
+    b4 = kchunk_bounds(130, 4)          # widths 64, 64, 2 -> 3 chunks
+    assert [w for w, _ in [(k1 - k0, 0) for k0, k1 in b4]] == [64, 64, 2]
+    assert transfers(b4, 2, mode="allgather") == [("allgather", [0, 1]), ("bcast", [2])]
+    # every chunk exactly once, in increasing order
+    for g in (2, 3, 4):
+        flat = [c for _, cs in transfers(kchunk_bounds(1000, 7), g, mode="allgather") for c in cs]
+        assert flat == sorted(flat) == list(range(len(kchunk_bounds(1000, 7))))
     o = panel_opts(148)
     assert o.plan_sms == 140 and o.num_ctas == 0 and list(o.reserved) == [0, 0, 0]
 
@@ -71,7 +91,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, M, N, K, chunks, q, owners=False):
+def _worker(rank, world, port, M, N, K, chunks, q, mode="root"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -83,7 +103,7 @@ def _worker(rank, world, port, M, N, K, chunks, q, owners=False):
         Bfull = torch.from_numpy(synth.matrix(K, N, seed=3, matrix_id=1))
         bounds = kchunk_bounds(K, chunks)
         B = torch.full((K, N), float("nan"))
-        for c in owned_chunks(len(bounds), world, rank, 0, owners):
+        for c in owned_chunks(len(bounds), world, rank, 0, mode):
             k0, k1 = bounds[c]
             B[k0:k1] = Bfull[k0:k1]
         events = []
@@ -99,7 +119,7 @@ def _worker(rank, world, port, M, N, K, chunks, q, owners=False):
                                  b.contiguous().numpy().reshape(-1), n, 0)
             c.copy_(torch.from_numpy(ref.astype(np.float32)))
 
-        C, info = gemm_rowpanel(A, B, chunks=chunks, owners=owners, gemm_fn=gemm_fn, signal_fn=signal_fn)
+        C, info = gemm_rowpanel(A, B, chunks=chunks, bcast=mode, gemm_fn=gemm_fn, signal_fn=signal_fn)
         assert info["chunks"] == len(bounds)
         q.put(("ok", rank, bool(torch.equal(B, Bfull)), events, C.numpy()))
     except Exception as e:   # surface worker failures to the parent
@@ -109,16 +129,17 @@ def _worker(rank, world, port, M, N, K, chunks, q, owners=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,M,N,K,chunks,owners", [(2, 256, 384, 96, 3, False), (3, 200, 300, 64, 2, False),
-                                                       (2, 130, 128, 33, 1, False), (3, 256, 200, 160, 5, True),
-                                                       (2, 300, 100, 130, 4, True)])
-def test_rowpanel_gloo(world, M, N, K, chunks, owners):
+@pytest.mark.parametrize("world,M,N,K,chunks,mode", [(2, 256, 384, 96, 3, "root"), (3, 200, 300, 64, 2, "root"),
+                                                     (2, 130, 128, 33, 1, "root"), (3, 256, 200, 160, 5, "owners"),
+                                                     (2, 300, 100, 130, 4, "owners"), (2, 256, 96, 256, 8, "allgather"),
+                                                     (3, 200, 64, 224, 7, "allgather"), (2, 100, 50, 130, 4, "allgather")])
+def test_rowpanel_gloo(world, M, N, K, chunks, mode):
     import oracle
     import synth
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, M, N, K, chunks, q, owners)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, M, N, K, chunks, q, mode)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=120) for _ in range(world)]

@@ -12,7 +12,7 @@ the float64 oracle, plus the gate's own contract:
   * gemm_rowpanel on a world-1 NCCL group (broadcast in K-row chunks, the
     signal kernel, the gated product on a plan of num_sms - 8) matches the
     oracle element by element and the ungated product bitwise, for chunk
-    counts 2 / 8 / 16, owners on and off, both paths; the host-buffer step
+    counts 2 / 8 / 16, every bcast mode, both paths; the host-buffer step
     (gemm_rowpanel_host) gives the same bits, with its PCIe byte accounting.
 """
 import os
@@ -157,13 +157,13 @@ def _sampled_cols(N, tile=256):
 
 
 @pytest.mark.parametrize("path", ["3xtf32", "ffma"])
-@pytest.mark.parametrize("chunks,owners", [(2, False), (8, True), (16, False)])
-def test_rowpanel_cuda_world1(path, chunks, owners):
+@pytest.mark.parametrize("chunks,mode", [(2, "root"), (8, "owners"), (16, "allgather")])
+def test_rowpanel_cuda_world1(path, chunks, mode):
     dist = _world1()
     M, N, K = 1024, 2048, 4096                    # a g=8 panel of n = 8192 in miniature
     A, B = _inputs(M, N, K, seed=11)
     dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
-    C, info = ldist.gemm_rowpanel(dA, dB, chunks=chunks, path=path, owners=owners)
+    C, info = ldist.gemm_rowpanel(dA, dB, chunks=chunks, path=path, bcast=mode)
     assert info["chunks"] == chunks and info["total_ms"] > 0 and info["bcast_ms"] > 0
     # bitwise the ungated product planned for the same SMs
     ref = lpy.gemm(dA, dB, path=path, opts=ldist.panel_opts(_sms()))
@@ -180,7 +180,7 @@ def test_rowpanel_cuda_world1(path, chunks, owners):
     assert err <= TOL
     # repeated steps raise the epoch and reuse the flags (no reset)
     for _ in range(3):
-        C2, _ = ldist.gemm_rowpanel(dA, dB, chunks=chunks, path=path, owners=owners, timings=False)
+        C2, _ = ldist.gemm_rowpanel(dA, dB, chunks=chunks, path=path, bcast=mode, timings=False)
     torch.cuda.synchronize()
     assert torch.equal(C2, ref)
 

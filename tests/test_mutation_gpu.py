@@ -2,10 +2,12 @@
 
 liblpy_mutant.so is the product library compiled with -DLPY_MUTATE_STAGE_RACE
 (paper_1405_7470_b200/_build.py): the FFMA consumers release a shared-memory
-stage to the TMA producer BEFORE reading it, and the 3xTF32 MMA issuer skips
-its wait for the stage's TMA + split transform.  The barrier protocol is
-otherwise intact, so nothing hangs -- the kernels just read stages that are
-being refilled or not yet written.
+stage to the TMA producer BEFORE reading it, and the 3xTF32 split-transform
+warps mark a stage ready for the MMA BEFORE writing its small parts.  Every
+barrier still receives its arrivals once per phase, so nothing hangs (a first
+3xTF32 mutant that skipped the MMA's wait instead let barrier phases overrun
+and hung) -- the kernels just read stages that are being refilled or not yet
+written.
 
 The detector is the check of tests/test_parity_gpu.py::test_repeatable_every_element
 (repeated runs bitwise equal, every element within the 1e-5 bound of a float64
@@ -51,7 +53,7 @@ DETECTOR = textwrap.dedent("""
 
 def _run(lib, path):
     r = subprocess.run([sys.executable, "-c", DETECTOR, lib, path], capture_output=True, text=True,
-                       timeout=300, cwd=ROOT)
+                       timeout=120, cwd=ROOT)
     line = [x for x in r.stdout.splitlines() if x.startswith("DETECTOR")]
     assert line, (r.stdout[-2000:], r.stderr[-2000:])
     return line[0]
