@@ -86,13 +86,65 @@ struct Params {
     int cluster_split;
     int ws_stride;   // float4 stride between a thread's partial float4s: 256 (interleaved) or 1 (LPY_FFMA_PARTIAL=contig, A/B)
     KGate gate;      // operands arriving in chunks of K (lpy_kgate): the producer waits per k-block
+    // Stream-K (sk_workers > 0; replaces the equal slices above): tiles
+    // [0, full_tiles) are one unit each; the remaining tiles' sk_iters =
+    // (num_tiles - full_tiles) * k_blocks k-block iterations are dealt out
+    // evenly to sk_workers workers (worker w: [floor(w W / P), floor((w+1) W / P))),
+    // a range at most one tile long, so it covers at most two pieces: unit
+    // full_tiles + piece * sk_stride + w (empty when it does not exist).  With
+    // a grid of sk_stride CTAs, CTA w runs worker w.  The pieces of a tile are
+    // summed in the kernel, in k order, by the piece that finishes last
+    // (tickets in sem); partials park in ws (slot = unit - full_tiles).
+    int full_tiles, sk_workers, sk_stride;
+    long long sk_iters;
+    int *sem;        // 2 x [num_tiles - full_tiles] ticket / written counters, zero on entry and exit
 };
 
+// Stream-K: the worker whose iteration range contains tail iteration x, and
+// the first iteration of worker w.
+__device__ __forceinline__ int sk_worker_of(long long x, const Params &p) {
+    return int(((x + 1) * p.sk_workers + p.sk_iters - 1) / p.sk_iters) - 1;
+}
+__device__ __forceinline__ long long sk_begin(int w, const Params &p) {
+    return (static_cast<long long>(w) * p.sk_iters) / p.sk_workers;
+}
+
+// Work unit u -> tile t and k-block range [kb0, kb1) (empty when kb0 >= kb1).
 __device__ __forceinline__ void unit_range(int u, const Params &p, int &t, int &kb0, int &kb1) {
+    if (p.sk_workers > 0) {
+        if (u < p.full_tiles) {
+            t = u; kb0 = 0; kb1 = p.k_blocks;
+            return;
+        }
+        const int su = u - p.full_tiles;
+        const int piece = su / p.sk_stride, w = su - piece * p.sk_stride;
+        t = p.full_tiles; kb0 = kb1 = 0;
+        if (w >= p.sk_workers) return;
+        const long long b0 = sk_begin(w, p), b1 = sk_begin(w + 1, p), kb = p.k_blocks;
+        const long long vt = b0 / kb + piece;
+        const long long lo = max(b0, vt * kb), hi = min(b1, (vt + 1) * kb);
+        if (lo >= hi) return;
+        t = p.full_tiles + int(vt);
+        kb0 = int(lo - vt * kb);
+        kb1 = int(hi - vt * kb);
+        return;
+    }
     t = u / p.splits;
     const int s = u - t * p.splits;
     kb0 = int((int64_t(s) * p.k_blocks) / p.splits);
     kb1 = int((int64_t(s + 1) * p.k_blocks) / p.splits);
+}
+// The pieces of stream-K tail tile vt in k order: count, and the unit slot
+// (index past full_tiles) of the i-th.
+__device__ __forceinline__ int sk_pieces(int vt, const Params &p) {
+    const long long kb = p.k_blocks;
+    return sk_worker_of((vt + 1) * kb - 1, p) - sk_worker_of(vt * kb, p) + 1;
+}
+__device__ __forceinline__ int sk_slot(int vt, int i, const Params &p) {
+    const long long kb = p.k_blocks;
+    const int w = sk_worker_of(vt * kb, p) + i;
+    const int piece = int(sk_begin(w, p) / kb) == vt ? 0 : 1;
+    return piece * p.sk_stride + w;
 }
 
 // Packed fp32 pairs for FFMA2.  c += a * b with c, b packed (lo, hi) pairs and
@@ -274,9 +326,11 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
     const int lm = lane >> 2, ln = lane & 3;
     int stage = 0;
     uint32_t phase = 0;
+    __shared__ int sk_last;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
         int t, kb0, kb1, tm, tn;
         unit_range(u, p, t, kb0, kb1);
+        if (kb0 >= kb1) continue;   // an empty stream-K unit
         tile_coords(t, p, tm, tn);
         // acc2[i][jp] = (acc(i, 2jp), acc(i, 2jp+1)): pairs along n, where one
         // LDS.128 of the MN-major B tile delivers adjacent columns
@@ -368,7 +422,106 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
             cluster_sync();   // peers done reading this CTA's partial
             continue;
         }
-        if constexpr (SPLIT) {
+        if (SPLIT && p.sk_workers > 0 && u >= p.full_tiles && !(kb0 == 0 && kb1 == p.k_blocks)) {
+            // ---------------------------------------- stream-K piece: fix-up in the kernel
+            // Each piece of a tail tile takes a ticket; all but the last park
+            // their partial (thread-interleaved, as the split-K slices do) and
+            // count themselves written; the last waits for those writes -- the
+            // writers already hold tickets, so they are running and the wait is
+            // bounded -- and sums the pieces in k order, its own from registers:
+            // ((p0 + p1) + p2) ..., with the own piece first or second the
+            // running sum starts from acc (p1 + p0 == p0 + p1 bitwise); a later
+            // own piece is parked and the sum rebuilt from memory.  The order is
+            // fixed by the decomposition, never by who finishes last.
+            const int vt = t - p.full_tiles;
+            const int npieces = sk_pieces(vt, p);
+            const int su = u - p.full_tiles;
+            const int me = su % p.sk_stride - sk_worker_of(static_cast<long long>(vt) * p.k_blocks, p);
+            int *arrive = p.sem + vt;
+            int *written = p.sem + (p.num_tiles - p.full_tiles) + vt;
+            constexpr int NV = 8 * JN / 2;                    // float4s per thread
+            auto slot_ptr = [&](int i) {
+                return reinterpret_cast<float4 *>(p.ws + int64_t(sk_slot(vt, i, p)) * (BM * BN)) + threadIdx.x;
+            };
+            auto park = [&](float4 *dst) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int jp = 0; jp < JN; jp += 2) {
+                        float lo0, hi0, lo1, hi1;
+                        unpack2(acc2[i][jp], lo0, hi0);
+                        unpack2(acc2[i][jp + 1], lo1, hi1);
+                        __stcg(dst + ((i * JN + jp) / 2) * (CWARPS * 32), make_float4(lo0, hi0, lo1, hi1));
+                    }
+            };
+            if (threadIdx.x == 0) sk_last = atomicAdd(arrive, 1) == npieces - 1;
+            named_bar_sync(1, CWARPS * 32);
+            if (!sk_last) {
+                park(slot_ptr(me));
+                __threadfence();
+                named_bar_sync(1, CWARPS * 32);
+                if (threadIdx.x == 0) atomicAdd(written, 1);
+                continue;
+            }
+            if (threadIdx.x == 0) {
+                while (ld_acquire_gpu(written) < npieces - 1) __nanosleep(64);
+                *arrive = 0;      // ready for the next launch (nobody else touches them now)
+                *written = 0;
+            }
+            named_bar_sync(1, CWARPS * 32);
+            __threadfence();
+            float acc[8][2 * JN];
+            int i0 = 0;
+            if (me >= 2) {
+                park(slot_ptr(me));
+                __threadfence_block();
+                const float4 *src = slot_ptr(0);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const float4 x = __ldcg(src + v * (CWARPS * 32));
+                    const int i = (2 * v) / JN, j = (4 * v) % (2 * JN);
+                    acc[i][j] = x.x; acc[i][j + 1] = x.y; acc[i][j + 2] = x.z; acc[i][j + 3] = x.w;
+                }
+                i0 = 1;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int jp = 0; jp < JN; ++jp) unpack2(acc2[i][jp], acc[i][2 * jp], acc[i][2 * jp + 1]);
+            }
+#pragma unroll 1
+            for (int q = i0; q < npieces; ++q) {
+                if (q == me && me < 2) continue;
+                const float4 *src = slot_ptr(q);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const float4 x = __ldcg(src + v * (CWARPS * 32));
+                    const int i = (2 * v) / JN, j = (4 * v) % (2 * JN);
+                    acc[i][j] += x.x; acc[i][j + 1] += x.y; acc[i][j + 2] += x.z; acc[i][j + 3] += x.w;
+                }
+            }
+            const int m0 = tm * BM, n0 = tn * BN;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int row = m0 + a_row(wm, lm, i);
+                if (row >= p.M) continue;
+                float *crow = p.C + int64_t(row) * p.ldc;
+#pragma unroll
+                for (int jq = 0; jq < JN / 2; ++jq) {
+                    const int col = n0 + b_col<JN>(wn, ln, jq * 4);
+                    if (p.c_vec && col + 3 < p.N) {
+                        *reinterpret_cast<float4 *>(crow + col) =
+                            make_float4(acc[i][jq * 4 + 0], acc[i][jq * 4 + 1], acc[i][jq * 4 + 2], acc[i][jq * 4 + 3]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (col + e < p.N) crow[col + e] = acc[i][jq * 4 + e];
+                    }
+                }
+            }
+            continue;
+        }
+        if (SPLIT && p.sk_workers == 0) {
             // ---------------------------------------- split-K: park the partial
             // Every slice stores its partial tile (each thread its own 8 x 2JN
             // values, contiguous) and the fix-up kernel (splitk_fixup) adds the
@@ -471,6 +624,51 @@ __global__ void __launch_bounds__(CWARPS * 32) splitk_fixup_kernel(const Params 
     }
 }
 
+// Stream-K for a ragged or under-filled last wave (the paper's "separate code
+// for edge and corner cases", as a fractional split): tiles
+// [0, (waves - 1) P) run whole, the last wave's rem tiles are dealt out as
+// rem * k_blocks k-block iterations over P' = min(P, iterations / 4) workers,
+// so it lasts rem / P' of a tile instead of a whole one.  Taken when its
+// modelled length -- the fix-up costs the last piece of a tile the reads of
+// the others' 128 KB partials and every other piece one write, ~2.6 us each
+// at the ~50 GB/s one SM pulls from L2 (round-1 measurement) -- beats the
+// split-K choice `splits` (with its fix-up kernel) by >= 3%.  Fixed by the shape and the planned SM
+// count (never by opts.num_ctas).  LPY_FFMA_STREAMK=0 disables it, =2 takes it
+// whenever it applies (A/B).
+struct StreamK { int full_tiles, workers; long long iters; };
+static StreamK choose_stream_k(int tiles, int k_blocks, int P, int splits, int bn) {
+    static const int mode = [] {
+        const char *e = getenv("LPY_FFMA_STREAMK");
+        return e ? atoi(e) : 1;
+    }();
+    StreamK r{tiles, 0, 0};
+    if (mode == 0 || tiles <= 0 || P <= 0 || k_blocks < 8) return r;
+    const int waves = (tiles + P - 1) / P;
+    const int rem = tiles - (waves - 1) * P;
+    if (rem == P) return r;
+    const long long iters = static_cast<long long>(rem) * k_blocks;
+    long long workers = P;
+    if (workers > iters / 4) workers = iters / 4;             // >= 4 k-blocks per worker
+    if (workers <= rem) return r;
+    const double kb_us = bn == 256 ? 4.2 : 2.1;               // one k-block of one tile at full FMA rate
+    const double tile_us = k_blocks * kb_us;
+    const double pieces = double(rem) * k_blocks / double(workers) < k_blocks ? 2.0 : 1.0;
+    const double fix = 2.6 * pieces / tile_us;                 // fix-up, in tiles
+    const double t_sk = (waves - 1) + double(rem) / double(workers) + fix;
+    const long long units = static_cast<long long>(tiles) * splits;
+    double t_split = double((units + P - 1) / P) / double(splits);
+    // the split-K alternative's own fix-up: none for a cluster split (a single
+    // wave, DSMEM), else the fix-up kernel re-reading every slice's partial
+    // (measured ~3 us + bytes at ~5 TB/s: 24 us at n = 2048 with 8 slices,
+    // 11 us on the ragged config with 3; profiles/r02_ffma_streamk.txt)
+    if (splits > 1 && units > P) t_split += (3.0 + double(units) * BM * bn * 4 / 5e6) / tile_us;
+    if (mode != 2 && t_sk > 0.97 * t_split) return r;
+    r.full_tiles = (waves - 1) * P;
+    r.workers = int(workers);
+    r.iters = iters;
+    return r;
+}
+
 template <bool AK, bool BKM, int BN>
 static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     using G = Geo<AK, BKM, BN>;
@@ -504,6 +702,21 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     prm.splits = choose_splits(prm.num_tiles, prm.k_blocks, kn.num_sms, min_kb, MAX_SPLITS);
     prm.num_units = prm.num_tiles * prm.splits;
     prm.ws = nullptr;
+    prm.sem = nullptr;
+    prm.full_tiles = prm.num_tiles;
+    prm.sk_workers = prm.sk_stride = 0;
+    prm.sk_iters = 0;
+    {
+        const StreamK sk = choose_stream_k(prm.num_tiles, prm.k_blocks, kn.num_sms, prm.splits, BN);
+        if (sk.workers > 0) {
+            prm.splits = 1;
+            prm.full_tiles = sk.full_tiles;
+            prm.sk_workers = sk.workers;
+            prm.sk_stride = kn.num_sms;
+            prm.sk_iters = sk.iters;
+            prm.num_units = sk.full_tiles + 2 * kn.num_sms;
+        }
+    }
     static const int ws_stride = [] {
         const char *v = getenv("LPY_FFMA_PARTIAL");
         return (v && v[0] == 'c') ? 1 : CWARPS * 32;
@@ -513,9 +726,10 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     int grid = kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms;
     if (grid > prm.num_units) grid = prm.num_units;
     if (grid < 1) grid = 1;
-    auto kern = prm.splits > 1 ? gemm_ffma_kernel<AK, BKM, BN, true> : gemm_ffma_kernel<AK, BKM, BN, false>;
+    const bool split_kernel = prm.splits > 1 || prm.sk_workers > 0;
+    auto kern = split_kernel ? gemm_ffma_kernel<AK, BKM, BN, true> : gemm_ffma_kernel<AK, BKM, BN, false>;
     static std::atomic<uint64_t> attr_done[2];
-    e = ensure_smem_attr(kern, int(G::SMEM_BYTES), attr_done[prm.splits > 1]);
+    e = ensure_smem_attr(kern, int(G::SMEM_BYTES), attr_done[split_kernel]);
     if (e != cudaSuccess) return e;
     // Cluster split: a single wave (one unit per CTA), S <= 8 (the portable
     // cluster size), as many tiles as clusters of S fit at once -> one cluster
@@ -568,7 +782,7 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
     // The split factor, from the shape and the device only (results never depend
     // on opts.num_ctas): choose_splits' S, or S/2 when clusters of S do not fit at
     // once but clusters of S/2 do (n = 512: 16 tiles, S = 8 -> 4).
-    bool cluster = cluster_on && fits(prm.splits);
+    bool cluster = prm.sk_workers == 0 && cluster_on && fits(prm.splits);
     if (cluster_on && !cluster && prm.splits >= 4 && fits(prm.splits / 2)) {
         prm.splits /= 2;
         prm.num_units = prm.num_tiles * prm.splits;
@@ -592,6 +806,19 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
         const size_t ws_bytes = size_t(prm.num_units) * BM * BN * 4;
         e = cudaMallocAsync(reinterpret_cast<void **>(&prm.ws), ws_bytes, s);
         if (e != cudaSuccess) return e;
+    } else if (prm.sk_workers > 0) {
+        // stream-K: a partial slot per (piece, worker) and the per-tail-tile
+        // ticket / written counters (zeroed here, left zero by the kernel)
+        const int tail = prm.num_tiles - prm.full_tiles;
+        const size_t ws_bytes = size_t(2) * prm.sk_stride * BM * BN * 4;
+        char *buf = nullptr;
+        e = cudaMallocAsync(reinterpret_cast<void **>(&buf), ws_bytes + size_t(tail) * 8, s);
+        if (e != cudaSuccess) return e;
+        prm.ws = reinterpret_cast<float *>(buf);
+        prm.sem = reinterpret_cast<int *>(buf + ws_bytes);
+        e = cudaMemsetAsync(prm.sem, 0, size_t(tail) * 8, s);
+        if (e != cudaSuccess) { cudaFreeAsync(buf, s); return e; }
+        if (grid > prm.sk_stride) grid = prm.sk_stride;
     }
 
     {

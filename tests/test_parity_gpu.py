@@ -277,6 +277,28 @@ def test_tail_split_and_tile_width_grid_invariance(path):
             run_gemm(A, B, path=path, opts=o)
 
 
+@pytest.mark.parametrize("M,N,K,plan", [(2048, 2048, 2048, 0), (1024, 3000, 2048, 0), (1024, 8192, 1024, 140),
+                                        (777, 1000, 1111, 0)])
+def test_ffma_stream_k_parity_and_grid_invariance(M, N, K, plan):
+    """FFMA stream-K (gemm_ffma.cu choose_stream_k): single-wave shapes whose
+    k-iterations are dealt out over every CTA (n = 2048: 128 tiles on 148
+    SMs), a ragged one, and the g=8 row panel planned for 140 SMs (a 1.83-wave
+    schedule whose tail is stream-K'd).  Element-wise within the bound of the
+    oracle, and bitwise equal whatever the grid (the decomposition follows the
+    shape and plan_sms only; the fix-up sums pieces in k order)."""
+    A, B = inputs(M, N, K, seed=M + N)
+    o = lpy.GemmOpts()
+    o.plan_sms = plan
+    ref, pad_ok = run_gemm(A, B, path="ffma", opts=o)
+    assert pad_ok
+    check(ref, A, B)
+    for ctas in (140, 97, 16):
+        o = lpy.GemmOpts()
+        o.plan_sms, o.num_ctas = plan, ctas
+        C, _ = run_gemm(A, B, path="ffma", opts=o)
+        assert np.array_equal(C, ref), ctas
+
+
 def test_concurrent_calls_on_two_streams():
     """Reentrancy (include/lpy.h): two host threads, two streams, split-K and
     tail-split products in flight at once, each with its own stream-ordered
