@@ -42,12 +42,12 @@ for lib in libs:
         with torch.cuda.graph(g, stream=s):
             for _ in range(reps):
                 lpy.gemm(a, b, out=C, path=path)
-        graphs[(lib, spec)] = (g, reps, err)
+        graphs[(lib, spec)] = (g, reps, err, (a, b, C))   # (tensors kept alive by the cases list too)
 res = {}
 for rnd in range(5):
     for spec, a, b, C in cases:
         for lib in libs:
-            g, reps, _ = graphs[(lib, spec)]
+            g, reps, _, _ = graphs[(lib, spec)]
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             g.replay()

@@ -206,3 +206,31 @@ def test_rowpanel_host_world1_and_emulated(path):
     info = ldist.gemm_rowpanel_host(hA, hB, hC, chunks=8, path=path, workspace=ws, emulate_world=8)
     assert info["h2d_bytes"] == 4 * (M * K + (K // 8) * N)
     assert torch.equal(hC, ref.cpu())
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("path", ["3xtf32", "ffma"])
+def test_rowpanel_full_size_emulated_g8(path):
+    """BASELINE config 4 at full size in the launch configuration bench.py
+    times for N>1 (here rank 0 of an emulated 8-rank split on a world-1 NCCL
+    group): the 1024 x 8192 x 8192 row panel through gemm_rowpanel (16 or 8
+    K-row chunks, the gated product planned for num_sms - 8).  Sampled
+    elements -- every 256-column tile boundary on the panel's first, middle
+    and last rows, plus 2000 random ones -- against the oracle, and the whole
+    panel bitwise the ungated product with the same plan."""
+    _world1()
+    n, rows = 8192, 1024
+    A = synth.matrix(rows, n, seed=0, matrix_id=synth.MATRIX_A)
+    B = synth.matrix(n, n, seed=0, matrix_id=synth.MATRIX_B)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    C, info = ldist.gemm_rowpanel(dA, dB, path=path)
+    ref = lpy.gemm(dA, dB, path=path, opts=ldist.panel_opts(_sms()))
+    torch.cuda.synchronize()
+    assert torch.equal(C, ref)
+    assert info["chunks"] == ldist.choose_kchunks(rows, n, path)
+    rng = np.random.default_rng(1)
+    cols = _sampled_cols(n)
+    ii = np.concatenate([np.repeat([0, 511, rows - 1], cols.size), rng.integers(0, rows, 2000)])
+    jj = np.concatenate([np.tile(cols, 3), rng.integers(0, n, 2000)])
+    Cref, D = oracle.gemm_elems(rows, n, n, A.reshape(-1), n, 0, B.reshape(-1), n, 0, ii, jj)
+    assert oracle.normalized_error(C.cpu().numpy()[ii, jj], Cref, D) <= TOL
