@@ -268,6 +268,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr int STAGES = C_::STAGES;
     static_assert(size_t(BM) * (BN + 4) * 4 <= size_t(STAGES) * C_::STAGE_BYTES,
                   "cluster-split staging must fit in the operand ring");
+    // A_small in TENSOR memory (narrow tiles, K-major A): the transform warps
+    // write each row's 16 small values straight into TMEM (lane = row) and the
+    // a_small * b_big MMA reads A from there ("TS" form) -- the A_small tile
+    // then never crosses the shared-memory port (neither the transform's write
+    // nor the MMA's read), which bounds the narrow tiles.  TMEM:
+    // the two partial accumulators at columns [0, BN) and [BN, 2 BN), A_small of
+    // stage s at 2 BN + 16 s.
+#ifdef LPY_TF32_NO_TMEMA
+    constexpr bool TA = false;       // (A/B build: A_small through shared memory everywhere)
+#else
+    constexpr bool TA = CG == 2 && !AMN && BN <= 192;
+#endif
+    static_assert(!TA || 2 * BN + 16 * STAGES <= int(TMEM_COLS), "A_small stages must fit in TMEM");
+    constexpr uint32_t acc_stride = TA ? uint32_t(BN) : 256u;
     constexpr uint32_t A_BYTES = C_::A_BYTES, RAW_BYTES = C_::RAW_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
 
     extern __shared__ uint8_t smem_raw[];
@@ -403,8 +417,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if (kb == kb0 && u == unit0 && lane == 0) TL(4);
                     if (kb == kb0 && su >= 0 && lane == 0 && su < p.sk_stride) TLC(6);
                     tc_fence_after();
-                    const uint32_t d = tmem + b * 256;
+                    const uint32_t d = tmem + b * acc_stride;
                     const uint64_t off = uint64_t(s) * STEP;
+                    const uint32_t a_tm = tmem + uint32_t(2 * BN + 16 * s);   // A_small of stage s (TA)
                     if (elect_one()) {
 #pragma unroll
                         for (int sub = 0; sub < BK / 8; ++sub) {
@@ -425,7 +440,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 umma_tf32_cg<CG>(d, a_big, b_big + SMALL, idesc, (first && sub == 0) ? 0u : 1u);
                                 umma_tf32_cg<CG>(d, a_big, b_big, idesc, 1u);
                             }
-                            umma_tf32_cg<CG>(d, a_big + SMALL, b_big, idesc, 1u);
+                            if constexpr (TA) {
+                                umma_tf32_ts_cg2(d, a_tm + 8 * sub, b_big, idesc, 1u);
+                            } else {
+                                umma_tf32_cg<CG>(d, a_big + SMALL, b_big, idesc, 1u);
+                            }
                         }
                         umma_commit_cg<CG>(&empty[s], pair_mask);
                         if (last) umma_commit_cg<CG>(&accf[b], pair_mask);
@@ -463,14 +482,43 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
                 const float4 *src = reinterpret_cast<const float4 *>(stages + s * STAGE_BYTES);
                 float4 *dst = reinterpret_cast<float4 *>(stages + s * STAGE_BYTES + RAW_BYTES);
+                if constexpr (TA) {
+                    // A: thread xt owns row xt (TMEM lane xt: warp 4 + q holds lanes
+                    // 32q..32q+31).  The raw K-major tile is 128 rows x 64 B under
+                    // the 64B swizzle: 16-byte chunk c of row r sits at c ^ ((r >> 1) & 3).
+                    uint32_t v[16];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const float4 q = src[xt * 4 + (c ^ ((xt >> 1) & 3))];
+                        v[4 * c + 0] = __float_as_uint(tf32_small(q.x));
+                        v[4 * c + 1] = __float_as_uint(tf32_small(q.y));
+                        v[4 * c + 2] = __float_as_uint(tf32_small(q.z));
+                        v[4 * c + 3] = __float_as_uint(tf32_small(q.w));
+                    }
+                    tmem_st_x16(tmem + (uint32_t((xt >> 5) * 32) << 16) + uint32_t(2 * BN + 16 * s), v);
+                    // B: as below, over the B part of the stage only
+                    constexpr int A4 = int(A_BYTES / 16), B_PER = int(C_::B_BYTES / 16) / (XFORM_WARPS * 32);
 #pragma unroll 4
-                for (int i = 0; i < PER_THREAD; ++i) {
-                    float4 v = src[xt + i * XFORM_WARPS * 32];
-                    v.x = tf32_small(v.x);
-                    v.y = tf32_small(v.y);
-                    v.z = tf32_small(v.z);
-                    v.w = tf32_small(v.w);
-                    dst[xt + i * XFORM_WARPS * 32] = v;
+                    for (int i = 0; i < B_PER; ++i) {
+                        float4 w = src[A4 + xt + i * XFORM_WARPS * 32];
+                        w.x = tf32_small(w.x);
+                        w.y = tf32_small(w.y);
+                        w.z = tf32_small(w.z);
+                        w.w = tf32_small(w.w);
+                        dst[A4 + xt + i * XFORM_WARPS * 32] = w;
+                    }
+                    tmem_st_wait();
+                    tc_fence_before();
+                } else {
+#pragma unroll 4
+                    for (int i = 0; i < PER_THREAD; ++i) {
+                        float4 v = src[xt + i * XFORM_WARPS * 32];
+                        v.x = tf32_small(v.x);
+                        v.y = tf32_small(v.y);
+                        v.z = tf32_small(v.z);
+                        v.w = tf32_small(v.w);
+                        dst[xt + i * XFORM_WARPS * 32] = v;
+                    }
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
@@ -506,7 +554,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (np == 0 && ept == 0) TL(6);
                 TR_T0(t_b);
                 tc_fence_after();
-                const uint32_t base = tmem + lane_base + b * 256 + half * EC;
+                const uint32_t base = tmem + lane_base + b * acc_stride + half * EC;
 #pragma unroll
                 for (int c = 0; c < EC; c += 32) {
                     uint32_t v0[16], v1[16];

@@ -21,10 +21,28 @@ for spec in shapes.split(";"):
     cases.append((spec, a, b, torch.empty(M, N, device="cuda")))
 
 
+import ctypes
+_libs = {}
+
+
 def use(lib):
-    lpy._lib = None
-    lpy.library_path = (lambda p: (lambda: p))(os.path.abspath(lib))
-    lpy.load_library()
+    """Bind `gemm` to lpy_gemm_f32_ex of this .so (raw ctypes: an older build may
+    lack symbols the current binding expects)."""
+    global gemm
+    if lib not in _libs:
+        L = ctypes.CDLL(os.path.abspath(lib))
+        i64, i32, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+        L.lpy_gemm_f32_ex.argtypes = [i64, i64, i64, vp, i64, i32, vp, i64, i32, vp, i64, i32, vp, i32, vp]
+        L.lpy_gemm_f32_ex.restype = i32
+        _libs[lib] = L
+    L = _libs[lib]
+    pid = lpy.PATHS[path]
+
+    def gemm(a, b, out):
+        la, lb, lc = lpy.operand_layout(a), lpy.operand_layout(b), lpy.operand_layout(out)
+        st = L.lpy_gemm_f32_ex(a.shape[0], b.shape[1], a.shape[1], a.data_ptr(), la[1], la[0], b.data_ptr(), lb[1],
+                               lb[0], out.data_ptr(), lc[1], lc[0], torch.cuda.current_stream().cuda_stream, pid, None)
+        assert st == 0, st
 
 
 graphs = {}
@@ -33,7 +51,7 @@ for lib in libs:
     for spec, a, b, C in cases:
         reps = 20 if a.shape[0] * b.shape[1] * a.shape[1] < 2e10 else 3
         for _ in range(3):
-            lpy.gemm(a, b, out=C, path=path)
+            gemm(a, b, C)
         torch.cuda.synchronize()
         ref = a[:32].double() @ b.double()
         err = ((C[:32].double() - ref).abs() / (a[:32].abs().double() @ b.abs().double())).max().item()
@@ -41,7 +59,7 @@ for lib in libs:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             for _ in range(reps):
-                lpy.gemm(a, b, out=C, path=path)
+                gemm(a, b, C)
         graphs[(lib, spec)] = (g, reps, err, (a, b, C))   # (tensors kept alive by the cases list too)
 res = {}
 for rnd in range(5):

@@ -10,6 +10,7 @@ import torch
 import paper_1405_7470_b200 as lpy
 
 tag = os.environ.get("TAG", os.environ.get("LPY_FFMA_STREAMK", "1"))
+PATH = os.environ.get("LPY_PATH", "ffma")
 CASES = [("cfg2 n1024 rr", 1024, 1024, 1024, "row", "row", 0), ("cfg2 n1024 rc", 1024, 1024, 1024, "row", "col", 0),
          ("cfg2 n1024 cr", 1024, 1024, 1024, "col", "row", 0), ("cfg2 n1024 cc", 1024, 1024, 1024, "col", "col", 0),
          ("cfg5 ld777", 1000, 3000, 777, "row", "col", 0), ("cfg5 ld780", 1000, 3000, 777, "row", "col", 3),
@@ -27,7 +28,7 @@ for name, M, N, K, la, lb, pad in CASES:
     a, b = operand(M, K, la, pad), operand(K, N, lb, pad)
     C = torch.empty(M, N, device="cuda")
     for _ in range(3):
-        lpy.gemm(a, b, out=C, path="ffma")
+        lpy.gemm(a, b, out=C, path=PATH)
     torch.cuda.synchronize()
     ref = a[:64].double() @ b.double()
     err = ((C[:64].double() - ref).abs() / (a[:64].abs().double() @ b.abs().double())).max().item()
@@ -35,7 +36,7 @@ for name, M, N, K, la, lb, pad in CASES:
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         for _ in range(20):
-            lpy.gemm(a, b, out=C, path="ffma")
+            lpy.gemm(a, b, out=C, path=PATH)
     ts = []
     for _ in range(5):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
