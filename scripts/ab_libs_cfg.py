@@ -64,7 +64,7 @@ for lib in libs:
 res = {}
 for rnd in range(5):
     for spec, a, b, C in cases:
-        for lib in libs:
+        for lib in libs[rnd % len(libs):] + libs[:rnd % len(libs)]:   # rotate: no first-in-round bias
             g, reps, _, _ = graphs[(lib, spec)]
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
