@@ -145,7 +145,7 @@ class _Flags:
         import torch
         self.flags = torch.zeros(FLAG_WORDS, dtype=torch.int32, device=device)
         self.epoch = 0
-        self.warm = False          # a step has run on this device (its kernels are loaded)
+        self.warm = set()          # (group, plan kinds) whose kernels a step has already launched
         self.lock = threading.Lock()
 
     def next_epoch(self) -> int:
@@ -298,19 +298,21 @@ def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=
                      else kgate_signal(fl.flags, c, epoch, stream=comm))
             ev["bcast"].record(comm)
 
-    # Enqueue order.  The first step on a device enqueues the whole chain first:
-    # every kernel it launches (NCCL's, the signal) is then loaded before the
+    # Enqueue order.  The first step of a kind (group, collectives used) on a
+    # device enqueues the whole chain first: every kernel it launches (NCCL's,
+    # the signal) is then loaded before the
     # product spins (lazy module loading would otherwise block those first
     # launches behind it, include/lpy.h).  Later steps enqueue the product
     # first, so it is running -- its first tiles waiting on chunk 0 -- while
     # the host is still enqueuing the chain.
-    if fl.warm:
+    key = (id(group), broadcast, tuple(sorted({kind for kind, _ in plan})), signal_fn is None)
+    if key in fl.warm:
         product()
         chain()
     else:
         chain()
         product()
-        fl.warm = True
+        fl.warm.add(key)
     caller.wait_stream(comm)
     if not timings:
         return out, {"events": ev, "chunks": len(bounds)}
