@@ -31,6 +31,7 @@ are torch.distributed.broadcast and the library's gated product and signal.
 from __future__ import annotations
 
 import math
+import os
 import threading
 
 RESERVE_SMS = 8          # SMs left to the broadcast's NCCL kernels + the signal kernel
@@ -305,8 +306,11 @@ def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=
     # launches behind it, include/lpy.h).  Later steps enqueue the product
     # first, so it is running -- its first tiles waiting on chunk 0 -- while
     # the host is still enqueuing the chain.
+    # (LPY_DIST_CHAIN_FIRST=1 keeps the chain-first order on every step: a
+    # profiler that serialises kernels -- ncu -- would otherwise run the product
+    # alone while its flags are still pending, and its deadlock detector traps)
     key = (id(group), broadcast, tuple(sorted({kind for kind, _ in plan})), signal_fn is None)
-    if key in fl.warm:
+    if key in fl.warm and os.environ.get("LPY_DIST_CHAIN_FIRST", "0") != "1":
         product()
         chain()
     else:
