@@ -6,9 +6,10 @@ on B200 through the C-ABI, BASELINE.json's metric
 
 One step = one whole distributed product over the n=8192 square workload
 (BASELINE config 4): at N=1 one lpy_gemm_f32 call; at N>1 each rank owns a
-row panel of A and C and B is broadcast from rank 0 with NCCL inside the step
-(chunked along N to overlap the per-block products).  `value` = 2 n^3 per
-step / max-over-ranks device time (strong scaling: total work fixed).
+row panel of A and C, B is broadcast from rank 0 with NCCL inside the step in
+chunks of K rows, and one K-gated product per rank consumes each chunk as it
+lands (dist.gemm_rowpanel).  `value` = 2 n^3 per step /
+max-over-ranks device time (strong scaling: total work fixed).
 
 Prints ONE JSON line on rank 0 (contract in the task statement; fields
 documented in DESIGN.md "Measurement").

@@ -68,6 +68,25 @@ def test_gated_ready_flags_bitwise_ungated(path, M, N, K, chunk_k):
 
 
 @pytest.mark.parametrize("path", ["ffma", "3xtf32"])
+@pytest.mark.parametrize("la,lb,lc", [(1, 0, 0), (0, 1, 0), (1, 1, 1), (0, 0, 1)])
+def test_gated_layouts_bitwise_ungated(path, la, lb, lc):
+    """The gate is on k, which every layout and the column-major-C swap
+    (C^T = B^T A^T) keep: any layout of A, B, C gives the ungated bits."""
+    M, N, K, chunk_k = 1000, 1100, 1024, 128
+    A, B = _inputs(M, N, K, seed=8)
+    dA = torch.from_numpy(A).cuda() if la == 0 else torch.from_numpy(A.T.copy()).cuda().t()
+    dB = torch.from_numpy(B).cuda() if lb == 0 else torch.from_numpy(B.T.copy()).cuda().t()
+    out = (torch.empty((M, N), device="cuda") if lc == 0 else torch.empty((N, M), device="cuda").t())
+    flags = torch.ones(K // chunk_k, dtype=torch.int32, device="cuda")
+    plan = _sms() - 8
+    lpy.gemm(dA, dB, out=out, path=path, opts=_opts(plan), gate=lpy.KGate(flags.data_ptr(), chunk_k, 1, 0))
+    ref = lpy.gemm(dA, dB, path=path, opts=_opts(plan))
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    check(out.cpu().numpy(), A, B)
+
+
+@pytest.mark.parametrize("path", ["ffma", "3xtf32"])
 @pytest.mark.parametrize("lc", [0, 1])
 def test_gate_orders_reads_after_arrival(path, lc):
     """B is NaN until a second stream writes chunk c and raises flags[c]
