@@ -76,11 +76,13 @@ def test_gated_layouts_bitwise_ungated(path, la, lb, lc):
     A, B = _inputs(M, N, K, seed=8)
     dA = torch.from_numpy(A).cuda() if la == 0 else torch.from_numpy(A.T.copy()).cuda().t()
     dB = torch.from_numpy(B).cuda() if lb == 0 else torch.from_numpy(B.T.copy()).cuda().t()
-    out = (torch.empty((M, N), device="cuda") if lc == 0 else torch.empty((N, M), device="cuda").t())
+    def new_out():   # (a column-major C is the transposed problem: compare like with like)
+        return torch.empty((M, N), device="cuda") if lc == 0 else torch.empty((N, M), device="cuda").t()
+    out, ref = new_out(), new_out()
     flags = torch.ones(K // chunk_k, dtype=torch.int32, device="cuda")
     plan = _sms() - 8
     lpy.gemm(dA, dB, out=out, path=path, opts=_opts(plan), gate=lpy.KGate(flags.data_ptr(), chunk_k, 1, 0))
-    ref = lpy.gemm(dA, dB, path=path, opts=_opts(plan))
+    lpy.gemm(dA, dB, out=ref, path=path, opts=_opts(plan))
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
     check(out.cpu().numpy(), A, B)
