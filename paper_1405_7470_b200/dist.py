@@ -344,7 +344,8 @@ class HostWorkspace:
 
 
 def gemm_rowpanel_host(A_panel, B, C_panel, group=None, root=0, chunks=None, path="auto", bcast="owners",
-                       reserve_sms=RESERVE_SMS, workspace=None, emulate_world=None, broadcast=True):
+                       reserve_sms=RESERVE_SMS, workspace=None, emulate_world=None, broadcast=True,
+                       device=None, gemm_fn=None):
     """End-to-end step from HOST buffers (pinned CPU tensors): the multi-GPU
     counterpart of lpy_gemm_f32_host.  Each rank uploads its A panel and only
     the K-row chunks of B it owns (chunk_owner: c mod world with bcast
@@ -359,13 +360,19 @@ def gemm_rowpanel_host(A_panel, B, C_panel, group=None, root=0, chunks=None, pat
     were that many ranks -- rank 0 uploads only its own chunks and the others
     are taken as already delivered (the workspace must hold them from an
     earlier call with emulate_world=None); the broadcast is a no-op.
+
+    device="cpu" (tests, gloo): the same plan on CPU "device" buffers -- the
+    uploads are plain copies of the owned chunks into a NaN-filled B, the
+    chunks go through gemm_rowpanel's CPU branch and `gemm_fn` computes the
+    panel -- so the ownership, the PCIe byte accounting and the broadcast plan
+    are exercised without a GPU (tests/test_dist.py).
     """
     import torch
     import torch.distributed as dist
 
     rows, K = A_panel.shape
     N = B.shape[1]
-    dev = torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     ws = workspace or _state.setdefault(("host_ws", str(dev)), HostWorkspace())
     world = dist.get_world_size(group) if broadcast else 1
     rank = dist.get_rank(group) if broadcast else 0
@@ -381,6 +388,18 @@ def gemm_rowpanel_host(A_panel, B, C_panel, group=None, root=0, chunks=None, pat
         bounds = kchunk_bounds(K, chunks or choose_kchunks(rows, K, resolved))
     check_kchunks(bounds, K)
     mine = set(owned_chunks(len(bounds), plan_world, rank, root, bcast))
+    if dev.type == "cpu":
+        dA = A_panel.clone()
+        dB = torch.full((K, N), float("nan"))
+        h2d_bytes = 4 * rows * K
+        for c in sorted(mine):
+            k0, k1 = bounds[c]
+            dB[k0:k1] = B[k0:k1]
+            h2d_bytes += 4 * (k1 - k0) * N
+        dC, _ = gemm_rowpanel(dA, dB, group=group, root=root, chunks=bounds, path=path, bcast=bcast,
+                              broadcast=world > 1, gemm_fn=gemm_fn)
+        C_panel.copy_(dC)
+        return {"h2d_bytes": h2d_bytes, "d2h_bytes": 4 * rows * N, "chunks": len(bounds), "B": dB}
     dA = ws.get("A", (rows, K), dev)
     dB = ws.get("B", (K, N), dev)
     dC = ws.get("C", (rows, N), dev)

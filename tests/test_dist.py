@@ -14,8 +14,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1405_7470_b200.dist import (check_kchunks, choose_kchunks, chunk_owner, gemm_rowpanel, kchunk_bounds,
-                                       owned_chunks, panel_bounds, panel_opts, transfers)
+from paper_1405_7470_b200.dist import (check_kchunks, choose_kchunks, chunk_owner, gemm_rowpanel, gemm_rowpanel_host,
+                                       kchunk_bounds, owned_chunks, panel_bounds, panel_opts, transfers)
 
 
 def test_panel_bounds_cover_rows_exactly():
@@ -160,3 +160,72 @@ def test_rowpanel_gloo(world, M, N, K, chunks, mode):
         panels[rank] = C
     C = np.concatenate([panels[r] for r in range(world)], axis=0)
     assert np.array_equal(C, Cref.astype(np.float32))
+
+
+def _host_worker(rank, world, port, M, N, K, chunks, q, mode):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import synth
+    try:
+        r0, r1 = panel_bounds(M, world, rank)
+        A = torch.from_numpy(synth.matrix(r1 - r0, K, seed=4, matrix_id=0, row0=r0))
+        bounds = kchunk_bounds(K, chunks)
+        # the host holds only this rank's chunks of B (the rest NaN): nothing else may be read
+        B = torch.full((K, N), float("nan"))
+        for c in owned_chunks(len(bounds), world, rank, 0, mode):
+            k0, k1 = bounds[c]
+            B[k0:k1] = torch.from_numpy(synth.matrix(k1 - k0, N, seed=4, matrix_id=1, row0=k0))
+        C = torch.full((r1 - r0, N), float("nan"))
+
+        def gemm_fn(a, b, c, _gate):
+            m, k = a.shape
+            n = b.shape[1]
+            ref, _ = oracle.gemm(m, n, k, a.contiguous().numpy().reshape(-1), k, 0,
+                                 b.contiguous().numpy().reshape(-1), n, 0)
+            c.copy_(torch.from_numpy(ref.astype(np.float32)))
+
+        info = gemm_rowpanel_host(A, B, C, chunks=chunks, bcast=mode, device="cpu", gemm_fn=gemm_fn)
+        q.put(("ok", rank, info["h2d_bytes"], info["d2h_bytes"], bool(torch.isnan(info["B"]).any()), C.numpy()))
+    except Exception as e:
+        q.put(("err", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,M,N,K,chunks,mode", [(2, 256, 96, 256, 8, "owners"), (3, 200, 64, 224, 7, "allgather"),
+                                                     (2, 130, 50, 130, 4, "owners")])
+def test_rowpanel_host_gloo(world, M, N, K, chunks, mode):
+    """The host-buffer step (dist.gemm_rowpanel_host) planned on CPU under
+    gloo: each rank "uploads" its A panel and only the chunks it owns -- its
+    host B holds nothing else (NaN) -- the plan completes B everywhere, the
+    panels concatenate to the oracle product, and the per-rank H2D bytes are
+    4 (rows K + owned chunk rows N): 4 (M K + K N) over all ranks, B once."""
+    import oracle
+    import synth
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_host_worker, args=(r, world, port, M, N, K, chunks, q, mode)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    errs = [r for r in results if r[0] == "err"]
+    assert not errs, errs
+    A = synth.matrix(M, K, seed=4, matrix_id=0)
+    B = synth.matrix(K, N, seed=4, matrix_id=1)
+    Cref, _ = oracle.gemm(M, N, K, A.reshape(-1), K, 0, B.reshape(-1), N, 0)
+    panels, h2d_total, d2h_total = {}, 0, 0
+    for _, rank, h2d, d2h, nan_left, C in results:
+        assert not nan_left, f"rank {rank}: B incomplete after the plan"
+        panels[rank] = C
+        h2d_total += h2d
+        d2h_total += d2h
+    C = np.concatenate([panels[r] for r in range(world)], axis=0)
+    assert np.array_equal(C, Cref.astype(np.float32))
+    assert h2d_total == 4 * (M * K + K * N) and d2h_total == 4 * M * N
