@@ -651,7 +651,7 @@ def main():
                          "rounds of N chunks are all-gathered (NCCL may run them as NVLS: --nccl-algo)")
     ap.add_argument("--nccl-algo", default="",
                     help="N>1: NCCL_ALGO for the run (e.g. NVLS, Ring); default: NCCL's own choice")
-    ap.add_argument("--reserve-sms", type=int, default=8,
+    ap.add_argument("--reserve-sms", type=int, default=16,
                     help="N>1: SMs the gated product leaves to the broadcast (dist.RESERVE_SMS)")
     ap.add_argument("--emulate-ranks", type=int, default=0,
                     help="diagnostics at N=1 with --force-dist: rank 0's panel of an N-rank split (not a bench value)")

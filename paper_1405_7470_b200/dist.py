@@ -34,7 +34,7 @@ import math
 import os
 import threading
 
-RESERVE_SMS = 8          # SMs left to the broadcast's NCCL kernels + the signal kernel
+RESERVE_SMS = 16         # SMs left to the broadcast's NCCL kernels + the signal kernel (profiles/r02_plan_sweep.txt)
 FLAG_WORDS = 4096        # flag array per device (chunks per call <= this)
 
 

@@ -80,7 +80,8 @@ def test_transfer_plan():
         flat = [c for _, cs in transfers(kchunk_bounds(1000, 7), g, mode="allgather") for c in cs]
         assert flat == sorted(flat) == list(range(len(kchunk_bounds(1000, 7))))
     o = panel_opts(148)
-    assert o.plan_sms == 140 and o.num_ctas == 0 and list(o.reserved) == [0, 0, 0]
+    assert o.plan_sms == 132 and o.num_ctas == 0 and list(o.reserved) == [0, 0, 0]
+    assert panel_opts(148, 8).plan_sms == 140
 
 
 def _free_port():

@@ -10,7 +10,7 @@ the float64 oracle, plus the gate's own contract:
   * a flag that never comes traps the kernel after timeout_ms (the deadlock
     detector), in a child process so this process's context survives;
   * gemm_rowpanel on a world-1 NCCL group (broadcast in K-row chunks, the
-    signal kernel, the gated product on a plan of num_sms - 8) matches the
+    signal kernel, the gated product on a plan of num_sms - 16) matches the
     oracle element by element and the ungated product bitwise, for chunk
     counts 2 / 8 / 16, every bcast mode, both paths; the host-buffer step
     (gemm_rowpanel_host) gives the same bits, with its PCIe byte accounting.
@@ -235,7 +235,7 @@ def test_rowpanel_full_size_emulated_g8(path):
     """BASELINE config 4 at full size in the launch configuration bench.py
     times for N>1 (here rank 0 of an emulated 8-rank split on a world-1 NCCL
     group): the 1024 x 8192 x 8192 row panel through gemm_rowpanel (16 or 8
-    K-row chunks, the gated product planned for num_sms - 8).  Sampled
+    K-row chunks, the gated product planned for num_sms - 16).  Sampled
     elements -- every 256-column tile boundary on the panel's first, middle
     and last rows, plus 2000 random ones -- against the oracle, and the whole
     panel bitwise the ungated product with the same plan."""
