@@ -52,6 +52,35 @@ for path, (M, N, K) in (("ffma", (1000, 1100, 600)), ("ffma", (1024, 1024, 1024)
     worst = max(worst, check(C, A, B))
 print(f"sanitize_small: split products within tolerance (worst {worst:.2e})")
 
+# round 2: FFMA stream-K (a single wave of 64 tiles over every SM, in-kernel
+# fix-up), the 3xTF32 stream-K tail (K >= 4096), the TMEM-A narrow tiles, and
+# the K-gated product with its flags raised by the signal kernel on a second stream
+for path, (M, N, K), plan in (("ffma", (1024, 3000, 2048), 0), ("3xtf32", (768, 1536, 4096), 16),
+                              ("3xtf32", (512, 768, 256), 0)):
+    A = synth.matrix(M, K, seed=6, matrix_id=0)
+    B = synth.matrix(K, N, seed=6, matrix_id=1)
+    o = lpy.GemmOpts()
+    o.plan_sms = plan
+    C, pad_ok = run_gemm(A, B, 0, 0, 0, path=path, opts=o)
+    assert pad_ok
+    worst = max(worst, check(C, A, B))
+for path in ("ffma", "3xtf32"):
+    M, N, K = 512, 1024, 1024
+    A = synth.matrix(M, K, seed=7, matrix_id=0)
+    B = synth.matrix(K, N, seed=7, matrix_id=1)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    flags = torch.zeros(4, dtype=torch.int32, device="cuda")
+    side = torch.cuda.Stream()
+    o = lpy.GemmOpts()
+    o.plan_sms = torch.cuda.get_device_properties(0).multi_processor_count - 16
+    C = lpy.gemm(dA, dB, path=path, opts=o, gate=lpy.KGate(flags.data_ptr(), 256, 1, 60000))
+    with torch.cuda.stream(side):
+        for c in range(4):
+            lpy.kgate_signal(flags, c, 1, stream=side)
+    torch.cuda.synchronize()
+    worst = max(worst, check(C.cpu().numpy(), A, B))
+print(f"sanitize_small: round-2 schedules within tolerance (worst {worst:.2e})")
+
 # saxpy edges (head / tail, misaligned x, x == y, strided)
 for n, offx, offy in ((1, 0, 0), (13, 1, 3), (1001, 2, 0), (4099, 0, 5)):
     x = synth.vector(n, 1, synth.VECTOR_X)
