@@ -65,13 +65,14 @@ def kchunk_bounds(K: int, chunks: int, align: int = 32) -> list[tuple[int, int]]
 def choose_kchunks(rows: int, K: int, path: str) -> int:
     """Broadcast chunks of B for a rank's (rows x N) panel: enough that the
     first chunk (the wait before the first tiles start) is a small share of
-    the step, few enough that NCCL's per-call overhead (~10-20 us) stays
-    hidden.  3xTF32 panels are fast (0.5 ms at 1024 x 8192 x 8192), so 16
-    chunks (512 rows, 16.8 MB at n = 8192); FFMA panels take ~2.3 ms and are
-    insensitive, 8; never chunks shorter than 256 rows of K."""
-    del rows
-    want = 16 if path != "ffma" else 8
-    return max(1, min(want, K // 256))
+    the step, few enough that the host's per-collective cost (a
+    torch.distributed call is ~10-30 us of host time, enqueued one after
+    another on the communication stream) stays well inside the broadcast it
+    overlaps: 8 chunks (1024 rows, 33.5 MB at n = 8192: the first arrives in
+    ~50 us at 700 GB/s, all 8 are enqueued within ~0.25 ms); never chunks
+    shorter than 256 rows of K."""
+    del rows, path
+    return max(1, min(8, K // 256))
 
 
 BCAST_MODES = ("root", "owners", "allgather")

@@ -48,7 +48,7 @@ def test_kchunk_bounds_cover_k_with_equal_chunks():
 
 
 def test_chunk_policy_and_ownership():
-    assert choose_kchunks(1024, 8192, "3xtf32") == 16
+    assert choose_kchunks(1024, 8192, "3xtf32") == 8
     assert choose_kchunks(1024, 8192, "ffma") == 8
     assert choose_kchunks(1024, 300, "3xtf32") == 1
     assert [chunk_owner(c, 4) for c in range(6)] == [0] * 6
