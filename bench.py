@@ -286,9 +286,17 @@ def time_path(args, path, rank, world, device, dist_on):
     del Bh
     C = torch.empty((rows, n), dtype=torch.float32, device=device)
 
+    graph = None
+    if dist_on and args.graph:
+        # the whole step (collectives + signals + gated product) as one CUDA graph
+        from paper_1405_7470_b200.dist import RowPanelGraph
+        graph = RowPanelGraph(A, B, C, chunks=bounds, path=path, reserve_sms=args.reserve_sms, bcast=mode)
+
     def step():
         if not dist_on:
             lpy.gemm(A, B, out=C, path=path)
+        elif graph is not None:
+            graph.replay()
         else:
             gemm_rowpanel(A, B, chunks=bounds, path=path, out=C, bcast=mode, reserve_sms=args.reserve_sms,
                           timings=False)
@@ -357,7 +365,7 @@ def time_path(args, path, rank, world, device, dist_on):
                  "gemm_ms": round(gemm_ms, 4), "bcast_bytes": nbytes,
                  "bcast_algbw_gbs": round(nbytes / (bcast_ms * 1e-3) / 1e9, 1), "chunks": len(bounds),
                  "chunk_k": bounds[0][1] - bounds[0][0], "plan_sms": opts.plan_sms,
-                 "reserve_sms": args.reserve_sms, "bcast": args.bcast}
+                 "reserve_sms": args.reserve_sms, "bcast": args.bcast, "graph": bool(args.graph)}
         dist.barrier()
         step()                      # the output parity checks below is a full step's
         torch.cuda.synchronize()
@@ -649,6 +657,9 @@ def main():
                     help="N>1: B starts on rank 0 and is broadcast (north_star), or starts sharded by "
                          "K-row chunks (chunk c on rank c mod N) and each owner broadcasts its chunks, or "
                          "rounds of N chunks are all-gathered (NCCL may run them as NVLS: --nccl-algo)")
+    ap.add_argument("--graph", action="store_true",
+                    help="N>1: capture the row-panel step (collectives, signals, gated product) as a CUDA graph "
+                         "and replay it (dist.RowPanelGraph): one launch per step instead of one host call per chunk")
     ap.add_argument("--nccl-algo", default="",
                     help="N>1: NCCL_ALGO for the run (e.g. NVLS, Ring); default: NCCL's own choice")
     ap.add_argument("--reserve-sms", type=int, default=16,

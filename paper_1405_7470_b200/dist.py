@@ -186,7 +186,7 @@ def panel_opts(sms: int, reserve_sms: int = RESERVE_SMS):
 def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=None,
                   reserve_sms=RESERVE_SMS, bcast="root", broadcast=True, comm_stream=None,
                   timings=True, bcast_fn=None, gather_fn=None, gemm_fn=None, signal_fn=None,
-                  before_chunk=None):
+                  before_chunk=None, flags=None, epoch=None):
     """One distributed product step on this rank: C_panel = A_panel @ B with B
     broadcast in K-row chunks while the gated product consumes them.
 
@@ -202,6 +202,9 @@ def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=
     before_chunk(c): optional hook run on the communication stream before
               chunk c's broadcast (the host-buffer step waits for the owner's
               upload there).
+    flags, epoch: an explicit flag array (int32 CUDA tensor) and epoch instead
+              of the device's shared ones (RowPanelGraph: a captured step resets
+              its own flags and always uses epoch 1).
     Returns (C_panel, info): with timings=True (CUDA) the step is synchronised
     and info = {"bcast_ms": start -> last chunk broadcast, "gemm_ms": start ->
     product done, "total_ms": start -> both done, "chunks": n} (the two overlap:
@@ -274,15 +277,18 @@ def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=
     dev = A_panel.device
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     fl = _flags_for(dev)
-    epoch = fl.next_epoch()
+    flag_t = flags if flags is not None else fl.flags
+    if epoch is None:
+        epoch = fl.next_epoch()
     caller = torch.cuda.current_stream(dev)
     comm = comm_stream or _comm_stream(dev)
-    ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "bcast", "gemm")}
+    capturing = torch.cuda.is_current_stream_capturing()
+    ev = {k: torch.cuda.Event(enable_timing=not capturing) for k in ("start", "bcast", "gemm")}
     # fork the communication stream off the caller's work so far -- recorded
     # BEFORE the product is enqueued, so the chain never waits for the product
     ev["start"].record(caller)
     comm.wait_event(ev["start"])
-    gate = KGate(fl.flags.data_ptr(), chunk_k, epoch, 0)
+    gate = KGate(flag_t.data_ptr(), chunk_k, epoch, 0)
     opts = panel_opts(sms, reserve_sms)
 
     def product():
@@ -297,7 +303,7 @@ def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=
     def chain():
         with torch.cuda.stream(comm):
             run_plan(lambda c: signal_fn(c, *bounds[c]) if signal_fn is not None
-                     else kgate_signal(fl.flags, c, epoch, stream=comm))
+                     else kgate_signal(flag_t, c, epoch, stream=comm))
             ev["bcast"].record(comm)
 
     # Enqueue order.  The first step of a kind (group, collectives used) on a
@@ -311,7 +317,7 @@ def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=
     # profiler that serialises kernels -- ncu -- would otherwise run the product
     # alone while its flags are still pending, and its deadlock detector traps)
     key = (id(group), broadcast, tuple(sorted({kind for kind, _ in plan})), signal_fn is None)
-    if key in fl.warm and os.environ.get("LPY_DIST_CHAIN_FIRST", "0") != "1":
+    if key in fl.warm and os.environ.get("LPY_DIST_CHAIN_FIRST", "0") != "1" and not capturing:
         product()
         chain()
     else:
@@ -319,12 +325,50 @@ def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=
         product()
         fl.warm.add(key)
     caller.wait_stream(comm)
-    if not timings:
+    if not timings or capturing:
         return out, {"events": ev, "chunks": len(bounds)}
     torch.cuda.synchronize(dev)
     b = ev["start"].elapsed_time(ev["bcast"])
     g = ev["start"].elapsed_time(ev["gemm"])
     return out, {"bcast_ms": b, "gemm_ms": g, "total_ms": max(b, g), "chunks": len(bounds)}
+
+
+class RowPanelGraph:
+    """One row-panel step (gemm_rowpanel) captured as a CUDA graph and replayed:
+    the chunk collectives, their signals and the gated product are enqueued by
+    ONE graph launch instead of ~10-30 us of host time per torch.distributed
+    call (the task's "capture launch-bound inner loops in CUDA graphs").  The
+    graph owns its flag array: its first node zeroes the flags, then the
+    communication branch (collectives + signals, epoch 1) and the product
+    branch run concurrently, the product spinning on the flags as in the eager
+    step.  A first eager step before the capture initialises the collectives'
+    communicator and loads every kernel.  Inputs and output are fixed at
+    construction (A_panel, B, out are reused by every replay).  NCCL
+    collectives inside CUDA graphs need the communicator to exist before the
+    capture, which the eager step guarantees."""
+
+    def __init__(self, A_panel, B, out, group=None, root=0, chunks=None, path="auto",
+                 reserve_sms=RESERVE_SMS, bcast="root"):
+        import torch
+        self.kw = dict(group=group, root=root, chunks=chunks, path=path, out=out, reserve_sms=reserve_sms,
+                       bcast=bcast)
+        self.A, self.B, self.out = A_panel, B, out
+        gemm_rowpanel(A_panel, B, timings=False, **self.kw)          # warm: comm init, kernel loads
+        torch.cuda.synchronize()
+        self.flags = torch.zeros(FLAG_WORDS, dtype=torch.int32, device=A_panel.device)
+        self.comm = torch.cuda.Stream(device=A_panel.device)
+        self.graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(device=A_panel.device)
+        cap.wait_stream(torch.cuda.current_stream(A_panel.device))
+        with torch.cuda.graph(self.graph, stream=cap):
+            self.flags.zero_()
+            _, self.info = gemm_rowpanel(A_panel, B, timings=False, comm_stream=self.comm, flags=self.flags,
+                                         epoch=1, **self.kw)
+        torch.cuda.synchronize()
+
+    def replay(self):
+        self.graph.replay()
+        return self.out
 
 
 class HostWorkspace:

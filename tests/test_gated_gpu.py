@@ -255,3 +255,27 @@ def test_rowpanel_full_size_emulated_g8(path):
     jj = np.concatenate([np.tile(cols, 3), rng.integers(0, n, 2000)])
     Cref, D = oracle.gemm_elems(rows, n, n, A.reshape(-1), n, 0, B.reshape(-1), n, 0, ii, jj)
     assert oracle.normalized_error(C.cpu().numpy()[ii, jj], Cref, D) <= TOL
+
+
+@pytest.mark.parametrize("path", ["3xtf32", "ffma"])
+def test_rowpanel_graph_replay(path):
+    """dist.RowPanelGraph: the step captured as a CUDA graph (flag reset ->
+    signals on one branch, the gated product spinning on them on the other)
+    replays bitwise the eager step, and inputs changed in place between
+    replays are picked up (the graph reads the same buffers)."""
+    _world1()
+    M, N, K = 1024, 2048, 4096
+    A, B = _inputs(M, N, K, seed=13)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    out = torch.empty((M, N), device="cuda")
+    ref, _ = ldist.gemm_rowpanel(dA, dB, chunks=8, path=path)
+    g = ldist.RowPanelGraph(dA, dB, out, chunks=8, path=path)
+    for _ in range(3):
+        out.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+    dA.mul_(-1.0)                                   # new inputs, same buffers: C must flip sign
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, -ref)
