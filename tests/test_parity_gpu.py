@@ -350,10 +350,13 @@ def test_host_entry_bench_config_sampled():
 
 
 @pytest.mark.parametrize("path", PATHS)
-@pytest.mark.parametrize("M,N,K", [(4096, 4096, 1024), (4096, 4096, 256), (2560, 2304, 1024)])
+@pytest.mark.parametrize("M,N,K", [(4096, 4096, 1024), (4096, 4096, 256), (2560, 2304, 1024),
+                                   (1024, 1024, 1024), (1000, 3000, 780), (2048, 2048, 2048)])
 def test_repeatable_every_element(path, M, N, K):
     """Race detector: shapes that run split-K / tail-split and full-width tiles,
-    repeated; every run bitwise equal to the first and EVERY element within the
+    the narrow TMEM-A tiles (n = 1024 BN=128 in 4-CTA clusters, the ragged
+    config's BN=192) and FFMA stream-K (n = 2048), repeated; every run bitwise
+    equal to the first and EVERY element within the
     bound of a float64 reference (cuBLAS DGEMM on the same inputs -- a library
     cross-check; the oracle pins exactness elsewhere).  A stage released while
     its last shared loads were still in flight showed up here as a few
