@@ -31,7 +31,7 @@ DETECTOR = textwrap.dedent("""
     if lib != "product":
         lpy.library_path = lambda: lib
     path = sys.argv[2]
-    M, N, K = 4096, 4096, 1024
+    M, N, K = (int(x) for x in sys.argv[3:6])
     g = torch.Generator(device="cuda")
     g.manual_seed(M + K)
     A = torch.rand(M, K, device="cuda", generator=g) * 2 - 1
@@ -51,19 +51,22 @@ DETECTOR = textwrap.dedent("""
 """).format(root=ROOT)
 
 
-def _run(lib, path):
-    r = subprocess.run([sys.executable, "-c", DETECTOR, lib, path], capture_output=True, text=True,
-                       timeout=120, cwd=ROOT)
+def _run(lib, path, shape):
+    r = subprocess.run([sys.executable, "-c", DETECTOR, lib, path, *map(str, shape)], capture_output=True,
+                       text=True, timeout=120, cwd=ROOT)
     line = [x for x in r.stdout.splitlines() if x.startswith("DETECTOR")]
     assert line, (r.stdout[-2000:], r.stderr[-2000:])
     return line[0]
 
 
 @pytest.mark.parametrize("path", ["ffma", "3xtf32"])
-def test_race_detector_passes_product_and_fails_mutant(path):
+@pytest.mark.parametrize("shape", [(4096, 4096, 1024), (1024, 1024, 1024)])
+def test_race_detector_passes_product_and_fails_mutant(path, shape):
+    """(4096 x 4096 x 1024: full-width tiles; 1024^3: the FFMA cluster split and
+    the 3xTF32 narrow tiles whose A_small goes through TMEM)"""
     import paper_1405_7470_b200._build as b
     assert os.path.exists(b.MUTANT_LIB), "liblpy_mutant.so not built (__graft_entry__.build())"
-    good = _run("product", path)
+    good = _run("product", path, shape)
     assert "PASS" in good, good
-    bad = _run(b.MUTANT_LIB, path)
+    bad = _run(b.MUTANT_LIB, path, shape)
     assert "FAIL" in bad, f"the race detector did not catch the stage race on {path}: {bad}"
