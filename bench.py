@@ -278,6 +278,8 @@ def time_path(args, path, rank, world, device, dist_on):
     rows = r1 - r0
     sms = torch.cuda.get_device_properties(device).multi_processor_count
     mode = args.bcast
+    from paper_1405_7470_b200.dist import comm_group, default_reserve
+    reserve = args.reserve_sms or default_reserve(path)
     bounds = kchunk_bounds(n, args.chunks or choose_kchunks(rows, n, path)) if dist_on else [(0, n)]
     mine = owned_chunks(len(bounds), world, rank, 0, mode) if dist_on else [0]
     Ah, Bh = host_inputs(n, r0, r1, [bounds[c] for c in mine] if dist_on and world > 1 else None)
@@ -290,7 +292,45 @@ def time_path(args, path, rank, world, device, dist_on):
     if dist_on and args.graph:
         # the whole step (collectives + signals + gated product) as one CUDA graph
         from paper_1405_7470_b200.dist import RowPanelGraph
-        graph = RowPanelGraph(A, B, C, chunks=bounds, path=path, reserve_sms=args.reserve_sms, bcast=mode)
+        graph = RowPanelGraph(A, B, C, chunks=bounds, path=path, reserve_sms=reserve, bcast=mode)
+
+    before_chunk = None
+    if dist_on and world == 1 and args.emulate_bcast_gbs > 0:
+        # Diagnostics (world 1): stand in for the broadcast's arrival of chunk c
+        # with, on the communication stream, a device-side wait and a copy of
+        # the chunk into B by `reserve_sms` persistent CTAs (liblpy_probe.so's
+        # persistent copy: the way a collective's channel CTAs move bytes, on
+        # the SMs the gated product leaves free, through HBM as a receive
+        # would), paced so the chunk rate does not exceed --emulate-bcast-gbs
+        # (0 < rate; a huge rate = copies back to back) -- a projection of a
+        # g-rank step, not a bench value.  (A first version copied with torch's
+        # elementwise kernel: its many small blocks on 16 SMs moved ~0.4 TB/s
+        # and measured that kernel rather than the overlap.)
+        import ctypes
+        probe = ctypes.CDLL(os.path.join(os.path.dirname(lpy.library_path()), "liblpy_probe.so"))
+        probe.lpy_probe_persistent_copy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,
+                                                    ctypes.c_int, ctypes.c_void_p]
+        probe.lpy_probe_bulk_copy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int,
+                                              ctypes.c_void_p]
+        bulk = os.environ.get("LPY_EMUL_COPY", "threads") == "bulk"   # TMA bulk copies instead of thread copies
+        Bsrc = B.clone()
+        clock_hz = 1.9e9
+
+        def before_chunk(c, _b=bounds):
+            k0, k1 = _b[c]
+            nbytes = 4 * (k1 - k0) * B.shape[1]
+            wait_s = nbytes / (args.emulate_bcast_gbs * 1e9)
+            if wait_s > 2e-6:
+                torch.cuda._sleep(int(wait_s * clock_hz))
+            ctas = max(1, reserve - 1)
+            if bulk:
+                rc = probe.lpy_probe_bulk_copy(B[k0:k1].data_ptr(), Bsrc[k0:k1].data_ptr(), nbytes, ctas,
+                                               torch.cuda.current_stream().cuda_stream)
+            else:
+                rc = probe.lpy_probe_persistent_copy(B[k0:k1].data_ptr(), Bsrc[k0:k1].data_ptr(),
+                                                     (k1 - k0) * B.shape[1], ctas,
+                                                     torch.cuda.current_stream().cuda_stream)
+            assert rc == 0, rc
 
     def step():
         if not dist_on:
@@ -298,8 +338,8 @@ def time_path(args, path, rank, world, device, dist_on):
         elif graph is not None:
             graph.replay()
         else:
-            gemm_rowpanel(A, B, chunks=bounds, path=path, out=C, bcast=mode, reserve_sms=args.reserve_sms,
-                          timings=False)
+            gemm_rowpanel(A, B, chunks=bounds, path=path, out=C, bcast=mode, reserve_sms=reserve,
+                          timings=False, before_chunk=before_chunk)
 
     for _ in range(args.warmup):
         step()
@@ -347,17 +387,18 @@ def time_path(args, path, rank, world, device, dist_on):
         # the two halves of a step, each timed alone (max over ranks): B's
         # chunked broadcast (4*K*N bytes from the owners) and this rank's
         # product planned for the same SMs, ungated (bitwise the gated one)
-        opts = panel_opts(sms, args.reserve_sms)
+        opts = panel_opts(sms, reserve)
         plan = transfers(bounds, world, 0, mode)
+        cg = comm_group(reserve)
 
         def comm_only():
             for kind, cs in plan:
                 if kind == "bcast":
                     k0, k1 = bounds[cs[0]]
-                    dist.broadcast(B[k0:k1], src=chunk_owner(cs[0], world, 0, mode))
+                    dist.broadcast(B[k0:k1], src=chunk_owner(cs[0], world, 0, mode), group=cg)
                 else:
                     p0, p1 = bounds[cs[rank]]
-                    dist.all_gather_into_tensor(B[bounds[cs[0]][0]:bounds[cs[-1]][1]], B[p0:p1])
+                    dist.all_gather_into_tensor(B[bounds[cs[0]][0]:bounds[cs[-1]][1]], B[p0:p1], group=cg)
         bcast_ms = timed(comm_only, reps)
         gemm_ms = timed(lambda: lpy.gemm(A, B, out=C, path=path, opts=opts), reps)
         nbytes = 4 * n * n
@@ -365,7 +406,8 @@ def time_path(args, path, rank, world, device, dist_on):
                  "gemm_ms": round(gemm_ms, 4), "bcast_bytes": nbytes,
                  "bcast_algbw_gbs": round(nbytes / (bcast_ms * 1e-3) / 1e9, 1), "chunks": len(bounds),
                  "chunk_k": bounds[0][1] - bounds[0][0], "plan_sms": opts.plan_sms,
-                 "reserve_sms": args.reserve_sms, "bcast": args.bcast, "graph": bool(args.graph)}
+                 "reserve_sms": reserve, "bcast": args.bcast, "graph": bool(args.graph),
+                 "emulate_bcast_gbs": args.emulate_bcast_gbs or None}
         dist.barrier()
         step()                      # the output parity checks below is a full step's
         torch.cuda.synchronize()
@@ -462,7 +504,7 @@ def time_e2e(args, path, rank, world, device, dist_on):
 
         def step():
             info = gemm_rowpanel_host(A, B, C, chunks=bounds, path=path, bcast=mode,
-                                      reserve_sms=args.reserve_sms, workspace=ws, emulate_world=emul)
+                                      reserve_sms=args.reserve_sms or None, workspace=ws, emulate_world=emul)
             return info["h2d_bytes"], info["d2h_bytes"]
 
     step()
@@ -660,10 +702,13 @@ def main():
     ap.add_argument("--graph", action="store_true",
                     help="N>1: capture the row-panel step (collectives, signals, gated product) as a CUDA graph "
                          "and replay it (dist.RowPanelGraph): one launch per step instead of one host call per chunk")
+    ap.add_argument("--emulate-bcast-gbs", type=float, default=0.0,
+                    help="diagnostics at N=1 with --force-dist: chunks 'arrive' at this rate (GB/s) through a "
+                         "paced copy-engine copy into B (a projection, not a bench value)")
     ap.add_argument("--nccl-algo", default="",
                     help="N>1: NCCL_ALGO for the run (e.g. NVLS, Ring); default: NCCL's own choice")
-    ap.add_argument("--reserve-sms", type=int, default=16,
-                    help="N>1: SMs the gated product leaves to the broadcast (dist.RESERVE_SMS)")
+    ap.add_argument("--reserve-sms", type=int, default=0,
+                    help="N>1: SMs the gated product leaves to the collectives (0: dist.default_reserve of the path)")
     ap.add_argument("--emulate-ranks", type=int, default=0,
                     help="diagnostics at N=1 with --force-dist: rank 0's panel of an N-rank split (not a bench value)")
     ap.add_argument("--force-dist", action="store_true",
@@ -706,9 +751,8 @@ def main():
         # where the launcher's rank check reads them
         if args.nccl_algo:
             os.environ["NCCL_ALGO"] = args.nccl_algo
-        # the gated product leaves --reserve-sms SMs to the collective: NCCL may not
-        # launch more CTAs than that (more would queue behind the product's grid)
-        os.environ.setdefault("NCCL_MAX_CTAS", str(max(1, args.reserve_sms)))
+        # (the chunk collectives run on dist.comm_group(reserve): a communicator
+        # whose maxCTAs keeps NCCL inside the SMs the gated product leaves)
         if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
             os.environ["NCCL_DEBUG"] = "INFO"
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")

@@ -185,7 +185,7 @@ lpy_status lpy_gemm_f32_ex(int64_t M, int64_t N, int64_t K,
  * SCHEDULING CONTRACT.  The product spins on the flags while occupying its
  * grid, so whatever sets them (the broadcast's NCCL kernels and the signal
  * kernel) must be able to run beside it: plan the product for fewer SMs than
- * the device has (opts.plan_sms; dist.py leaves 16 free) or set the flags from
+ * the device has (opts.plan_sms; dist.py leaves 32 free) or set the flags from
  * a copy engine / the host.  Every kernel that sets flags must also be LOADED
  * before the product is launched: under CUDA's lazy module loading a kernel's
  * first launch loads its code and waits for the device, i.e. for the spinning

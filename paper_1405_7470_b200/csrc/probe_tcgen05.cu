@@ -421,3 +421,101 @@ extern "C" int lpy_probe_x2_rate(int kind, float *out, int iters, int blocks, in
     }
     return int(cudaGetLastError());
 }
+
+// ---------------------------------------------------------------- persistent copy (diagnostics)
+// dst := src over n floats by exactly `ctas` CTAs of 512 threads, each thread
+// keeping four 16-byte loads in flight in a grid-stride loop: a stand-in for
+// a collective's persistent channel CTAs when bench.py --emulate-bcast-gbs
+// projects the row-panel step on one GPU (how many bytes `ctas` SMs move
+// while the gated product holds the rest).
+namespace lpy {
+namespace probe {
+__global__ void __launch_bounds__(512) persistent_copy_kernel(float4 *dst, const float4 *src, long long n4) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n4; i += 4 * stride) {
+        const float4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+        dst[i] = a; dst[i + stride] = b; dst[i + 2 * stride] = c; dst[i + 3 * stride] = d;
+    }
+    for (; i < n4; i += stride) dst[i] = src[i];
+}
+}  // namespace probe
+}  // namespace lpy
+
+extern "C" int lpy_probe_persistent_copy(float *dst, const float *src, long long n, int ctas, void *stream) {
+    // n must be a multiple of 4 and both pointers 16-byte aligned (diagnostics only)
+    lpy::probe::persistent_copy_kernel<<<ctas, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<float4 *>(dst), reinterpret_cast<const float4 *>(src), n / 4);
+    return int(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------- TMA bulk copy (diagnostics)
+// dst := src (bytes, multiple of 16, 16-byte aligned) by `ctas` CTAs whose one
+// elected thread streams 32 KB pieces global -> shared -> global with
+// cp.async.bulk (4 buffers in flight): how many bytes a few SMs move when the
+// copy engine of the SM (TMA) does the work instead of threads' loads/stores.
+namespace lpy {
+namespace probe {
+constexpr int BULK_BUF = 32 * 1024, BULK_NBUF = 6;
+__global__ void __launch_bounds__(32) bulk_copy_kernel(char *dst, const char *src, long long bytes) {
+    extern __shared__ __align__(128) unsigned char bsm[];
+    __shared__ __align__(8) unsigned long long bar[BULK_NBUF];
+    if (threadIdx.x != 0) return;
+    for (int b = 0; b < BULK_NBUF; ++b)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&bar[b])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const long long pieces = (bytes + BULK_BUF - 1) / BULK_BUF;
+    unsigned phase[BULK_NBUF] = {0, 0, 0, 0, 0, 0};
+    int issued = 0;
+    long long mine[BULK_NBUF];
+    for (long long p = blockIdx.x; p < pieces; p += gridDim.x) {
+        const int b = issued % BULK_NBUF;
+        if (issued >= BULK_NBUF) {
+            // buffer b: its previous piece must be loaded and stored out before reuse
+            const long long q = mine[b];
+            const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar[b]);
+            asm volatile("{\n\t.reg .pred P;\n\tW: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t@!P bra W;\n\t}"
+                         ::"r"(sb), "r"(phase[b]) : "memory");
+            phase[b] ^= 1;
+            const long long qb = q * BULK_BUF, n = min((long long)BULK_BUF, bytes - qb);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         ::"l"(dst + qb), "r"((unsigned)__cvta_generic_to_shared(bsm + b * BULK_BUF)), "r"((unsigned)n)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(0) : "memory");
+        }
+        const long long pb = p * BULK_BUF, n = min((long long)BULK_BUF, bytes - pb);
+        const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar[b]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"((unsigned)n) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"((unsigned)__cvta_generic_to_shared(bsm + b * BULK_BUF)), "l"(src + pb), "r"((unsigned)n), "r"(sb)
+                     : "memory");
+        mine[b] = p;
+        ++issued;
+    }
+    // drain
+    const int live = issued < BULK_NBUF ? issued : BULK_NBUF;
+    for (int j = 0; j < live; ++j) {
+        const int b = (issued - live + j) % BULK_NBUF;
+        const long long q = mine[b];
+        const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar[b]);
+        asm volatile("{\n\t.reg .pred P;\n\tW: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t@!P bra W;\n\t}"
+                     ::"r"(sb), "r"(phase[b]) : "memory");
+        const long long qb = q * BULK_BUF, n = min((long long)BULK_BUF, bytes - qb);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(dst + qb), "r"((unsigned)__cvta_generic_to_shared(bsm + b * BULK_BUF)), "r"((unsigned)n)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+}  // namespace probe
+}  // namespace lpy
+
+extern "C" int lpy_probe_bulk_copy(void *dst, const void *src, long long bytes, int ctas, void *stream) {
+    const int smem = lpy::probe::BULK_BUF * lpy::probe::BULK_NBUF;
+    cudaFuncSetAttribute(lpy::probe::bulk_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    lpy::probe::bulk_copy_kernel<<<ctas, 32, smem, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<char *>(dst), static_cast<const char *>(src), bytes);
+    return int(cudaGetLastError());
+}

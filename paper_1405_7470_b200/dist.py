@@ -22,7 +22,8 @@ per-block products that each under-fill the GPU.
 
 Scheduling contract: the product spins on flags while it holds its SMs, so it
 is planned for `num_sms - reserve_sms` SMs (opts.plan_sms), leaving the rest to
-NCCL's broadcast kernels and the signal kernel.
+NCCL's collective kernels (capped at reserve_sms - 1 CTAs through the
+communicator's maxCTAs, comm_group) and the signal kernel.
 
 Pieces are injectable (`bcast_fn`, `gemm_fn`, `signal_fn`) so the orchestration
 runs on CPU under gloo in the tests (tests/test_dist.py); on CUDA the defaults
@@ -34,7 +35,17 @@ import math
 import os
 import threading
 
-RESERVE_SMS = 16         # SMs left to the broadcast's NCCL kernels + the signal kernel (profiles/r02_plan_sweep.txt)
+RESERVE_SMS = {"3xtf32": 32, "ffma": 8}   # SMs left to the collectives per path (profiles/r02_bcast_emul.txt)
+
+
+def default_reserve(path: str) -> int:
+    """SMs a rank's gated product leaves to the chunk collectives.  Measured on
+    one GPU with each chunk moved through HBM by persistent CTAs on the free SMs
+    (the per-rank work of a ring broadcast; profiles/r02_bcast_emul.txt): the
+    3xTF32 panel (0.5 ms) is paced by those copies below ~32 SMs (step 0.78 /
+    0.73 / 0.65 / 0.64 ms with 16 / 24 / 32 / 40), the FFMA panel (2.4 ms) by its
+    own product (2.55 / 2.57 / 2.83 / 3.23 ms with 8 / 16 / 24 / 32)."""
+    return RESERVE_SMS.get(path, 32)
 FLAG_WORDS = 4096        # flag array per device (chunks per call <= this)
 
 
@@ -174,7 +185,28 @@ def _comm_stream(device):
     return _state[key]
 
 
-def panel_opts(sms: int, reserve_sms: int = RESERVE_SMS):
+def comm_group(reserve_sms: int, group=None):
+    """The NCCL process group the chunk collectives run on: the ranks of
+    `group` (default: all), with NCCL told to launch at most reserve_sms - 1
+    CTAs per collective (ncclConfig maxCTAs) -- the SMs the gated product
+    leaves, less one for the signal kernel -- so a collective never queues CTAs
+    behind the spinning product.  Created once per (ranks, reserve): all ranks
+    must reach the first call for a given reserve together (new_group is
+    collective), as the row-panel step guarantees."""
+    import torch.distributed as dist
+    if dist.get_backend(group) != "nccl":
+        return group
+    ranks = tuple(dist.get_process_group_ranks(group)) if group is not None else tuple(range(dist.get_world_size()))
+    key = ("comm_group", ranks, int(reserve_sms))
+    if key not in _state:
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.config.max_ctas = max(1, int(reserve_sms) - 1)
+        opts.config.min_ctas = 1
+        _state[key] = dist.new_group(ranks=list(ranks), backend="nccl", pg_options=opts)
+    return _state[key]
+
+
+def panel_opts(sms: int, reserve_sms: int = 32):
     """GemmOpts of the gated panel product: planned for the SMs the broadcast
     leaves it (results depend on plan_sms, never on the grid)."""
     from . import GemmOpts
@@ -184,7 +216,7 @@ def panel_opts(sms: int, reserve_sms: int = RESERVE_SMS):
 
 
 def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=None,
-                  reserve_sms=RESERVE_SMS, bcast="root", broadcast=True, comm_stream=None,
+                  reserve_sms=None, bcast="root", broadcast=True, comm_stream=None,
                   timings=True, bcast_fn=None, gather_fn=None, gemm_fn=None, signal_fn=None,
                   before_chunk=None, flags=None, epoch=None):
     """One distributed product step on this rank: C_panel = A_panel @ B with B
@@ -195,6 +227,9 @@ def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=
               owner (chunk_owner: `root` with bcast="root", else c mod world)
               on entry and on every rank on exit.
     bcast   : "root" | "owners" | "allgather" (chunk_owner, transfers).
+    reserve_sms: SMs the product leaves to the collectives (None: default_reserve
+              of the path); on NCCL the collectives run on comm_group(reserve_sms),
+              whose communicator launches at most reserve_sms - 1 CTAs.
     out     : optional (rows_r, N) fp32 output (row- or column-major).
     chunks  : number of K-row chunks (None: choose_kchunks) or explicit
               kchunk_bounds-style [(k0, k1), ...] ranges (each >= 32 rows but
@@ -234,6 +269,10 @@ def gemm_rowpanel(A_panel, B, group=None, root=0, chunks=None, path="auto", out=
     chunk_k = check_kchunks(bounds, K)
     if len(bounds) > FLAG_WORDS:
         raise ValueError(f"at most {FLAG_WORDS} chunks")
+    if reserve_sms is None:
+        reserve_sms = default_reserve(resolved)
+    if A_panel.is_cuda and broadcast and bcast_fn is None and gather_fn is None:
+        group = comm_group(reserve_sms, group)
     world = dist.get_world_size(group) if broadcast else 1
     # a broadcast among one rank moves nothing: skipped (the chunks are still
     # signalled, so a world-1 step runs the same gated product)
@@ -348,7 +387,7 @@ class RowPanelGraph:
     capture, which the eager step guarantees."""
 
     def __init__(self, A_panel, B, out, group=None, root=0, chunks=None, path="auto",
-                 reserve_sms=RESERVE_SMS, bcast="root"):
+                 reserve_sms=None, bcast="root"):
         import torch
         self.kw = dict(group=group, root=root, chunks=chunks, path=path, out=out, reserve_sms=reserve_sms,
                        bcast=bcast)
@@ -389,7 +428,7 @@ class HostWorkspace:
 
 
 def gemm_rowpanel_host(A_panel, B, C_panel, group=None, root=0, chunks=None, path="auto", bcast="owners",
-                       reserve_sms=RESERVE_SMS, workspace=None, emulate_world=None, broadcast=True,
+                       reserve_sms=None, workspace=None, emulate_world=None, broadcast=True,
                        device=None, gemm_fn=None):
     """End-to-end step from HOST buffers (pinned CPU tensors): the multi-GPU
     counterpart of lpy_gemm_f32_host.  Each rank uploads its A panel and only

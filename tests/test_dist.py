@@ -15,7 +15,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_1405_7470_b200.dist import (check_kchunks, choose_kchunks, chunk_owner, gemm_rowpanel, gemm_rowpanel_host,
-                                       kchunk_bounds, owned_chunks, panel_bounds, panel_opts, transfers)
+                                       default_reserve, kchunk_bounds, owned_chunks, panel_bounds, panel_opts,
+                                       transfers)
 
 
 def test_panel_bounds_cover_rows_exactly():
@@ -79,8 +80,9 @@ def test_transfer_plan():
     for g in (2, 3, 4):
         flat = [c for _, cs in transfers(kchunk_bounds(1000, 7), g, mode="allgather") for c in cs]
         assert flat == sorted(flat) == list(range(len(kchunk_bounds(1000, 7))))
-    o = panel_opts(148)
-    assert o.plan_sms == 132 and o.num_ctas == 0 and list(o.reserved) == [0, 0, 0]
+    assert default_reserve("3xtf32") == 32 and default_reserve("ffma") == 8
+    o = panel_opts(148, default_reserve("3xtf32"))
+    assert o.plan_sms == 116 and o.num_ctas == 0 and list(o.reserved) == [0, 0, 0]
     assert panel_opts(148, 8).plan_sms == 140
 
 

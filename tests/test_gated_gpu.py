@@ -10,7 +10,7 @@ the float64 oracle, plus the gate's own contract:
   * a flag that never comes traps the kernel after timeout_ms (the deadlock
     detector), in a child process so this process's context survives;
   * gemm_rowpanel on a world-1 NCCL group (broadcast in K-row chunks, the
-    signal kernel, the gated product on a plan of num_sms - 16) matches the
+    signal kernel, the gated product on a plan of num_sms - dist.default_reserve) matches the
     oracle element by element and the ungated product bitwise, for chunk
     counts 2 / 8 / 16, every bcast mode, both paths; the host-buffer step
     (gemm_rowpanel_host) gives the same bits, with its PCIe byte accounting.
@@ -187,7 +187,7 @@ def test_rowpanel_cuda_world1(path, chunks, mode):
     C, info = ldist.gemm_rowpanel(dA, dB, chunks=chunks, path=path, bcast=mode)
     assert info["chunks"] == chunks and info["total_ms"] > 0 and info["bcast_ms"] > 0
     # bitwise the ungated product planned for the same SMs
-    ref = lpy.gemm(dA, dB, path=path, opts=ldist.panel_opts(_sms()))
+    ref = lpy.gemm(dA, dB, path=path, opts=ldist.panel_opts(_sms(), ldist.default_reserve(path)))
     torch.cuda.synchronize()
     assert torch.equal(C, ref)
     # B survived its (world-1) broadcast
@@ -217,7 +217,7 @@ def test_rowpanel_host_world1_and_emulated(path):
     ws = ldist.HostWorkspace()
     info = ldist.gemm_rowpanel_host(hA, hB, hC, chunks=8, path=path, workspace=ws)
     ref = lpy.gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), path=path,
-                   opts=ldist.panel_opts(_sms()))
+                   opts=ldist.panel_opts(_sms(), ldist.default_reserve(path)))
     torch.cuda.synchronize()
     assert torch.equal(hC, ref.cpu())
     assert info["h2d_bytes"] == 4 * (M * K + K * N) and info["d2h_bytes"] == 4 * M * N
@@ -235,7 +235,7 @@ def test_rowpanel_full_size_emulated_g8(path):
     """BASELINE config 4 at full size in the launch configuration bench.py
     times for N>1 (here rank 0 of an emulated 8-rank split on a world-1 NCCL
     group): the 1024 x 8192 x 8192 row panel through gemm_rowpanel (16 or 8
-    K-row chunks, the gated product planned for num_sms - 16).  Sampled
+    K-row chunks, the gated product planned for num_sms - dist.default_reserve).  Sampled
     elements -- every 256-column tile boundary on the panel's first, middle
     and last rows, plus 2000 random ones -- against the oracle, and the whole
     panel bitwise the ungated product with the same plan."""
@@ -245,7 +245,7 @@ def test_rowpanel_full_size_emulated_g8(path):
     B = synth.matrix(n, n, seed=0, matrix_id=synth.MATRIX_B)
     dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
     C, info = ldist.gemm_rowpanel(dA, dB, path=path)
-    ref = lpy.gemm(dA, dB, path=path, opts=ldist.panel_opts(_sms()))
+    ref = lpy.gemm(dA, dB, path=path, opts=ldist.panel_opts(_sms(), ldist.default_reserve(path)))
     torch.cuda.synchronize()
     assert torch.equal(C, ref)
     assert info["chunks"] == ldist.choose_kchunks(rows, n, path)
