@@ -907,9 +907,10 @@ static TailSplit tail_split(int num_tiles, int k_blocks, int pairs, const Cluste
 // Tile width for a CTA-pair product (256-row tiles): the BN in {256, 192, 128}
 // minimising the modelled time of the schedule it gives on `pairs` persistent
 // CTA pairs: (unit waves) x (k-blocks per unit) x BN / (the kernel's measured
-// per-flop efficiency at that width relative to 256: 0.86 for 192, 0.69 for
+// per-flop efficiency at that width relative to 256: 0.94 for 192, 0.80 for
 // 128 at n = 8192 -- narrower MMAs leave the fixed per-k-block work (the A
-// tile's TMA and split) less time to hide in; profiles/r01_tf32_bn_sweep.txt),
+// tile's TMA and split) less time to hide in; profiles/r02_tf32_bn_sweep.txt,
+// with A_small in TMEM for the narrow widths; round 1 measured 0.86 / 0.69),
 // over the useful columns; narrower wins only by > 3%.  n >= 4096 -> 256;
 // n = 1024 -> 128 (32 tiles instead of 16); the ragged config -> 192 (64 tiles
 // instead of 48).
@@ -919,7 +920,7 @@ int choose_bn(int M, int N, int K, int pairs, const ClusterCaps &caps) {
     auto cost = [&](int bn) {
         const int64_t tn = (N + bn - 1) / bn, tiles = tm * tn;
         const TailSplit ts = tail_split(int(tiles), kb, pairs, caps);
-        const double kern = bn == 256 ? 1.0 : bn == 192 ? 0.86 : 0.69;
+        const double kern = bn == 256 ? 1.0 : bn == 192 ? 0.94 : 0.80;
         return ts.waves * bn / kern * double(tn * bn) / double(N);
     };
     int best = 256;
