@@ -36,6 +36,16 @@
 //                ragged K).
 // Operand smem layouts: K-major tiles use the 64B swizzle (16 fp32 per row);
 // MN-major tf32 tiles must use SWIZZLE_128B_BASE32B (TMA "128B_ATOM_32B").
+// Narrow tiles (BN <= 192) with a K-major A keep A_small in TENSOR memory: the
+// transform warps write each row's 16 small values with tcgen05.st and the
+// a_small * b_big MMA reads A from TMEM (TS form), so that tile never crosses
+// the shared-memory port.
+// Around the k loop: ragged last waves are stream-K'd (tail_split: the tail's
+// k-iterations dealt over every planned pair, pieces summed in k order by the
+// last to finish); a single under-filled wave is split inside a cluster and
+// summed through DSMEM; and an optional K-gate (lpy_gemm_f32_gated) makes the
+// producer wait for each chunk of K to be flagged as arrived before loading it
+// -- the multi-GPU row-panel product consuming B while it is broadcast.
 #include <cstdlib>
 #include <mutex>
 #include "lpy_internal.h"

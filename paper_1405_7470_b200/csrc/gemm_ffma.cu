@@ -33,6 +33,14 @@
 // used as a layout change -- before the consumers see it.
 // Accumulation is fp32 FFMA (RN) with k ascending per element, identical for
 // every layout.
+//
+// Under-filled grids (the paper's "separate code for edge and corner cases",
+// P:524-528): a single wave of too few tiles splits K inside a thread-block
+// cluster (DSMEM reduction); a ragged last wave is stream-K'd (its k-iterations
+// dealt over every planned SM, pieces summed in k order by the last to finish,
+// in the consumer warps); otherwise split-K slices and a fix-up kernel --
+// whichever choose_stream_k's model says is shortest.  The producer honours
+// the K-gate of lpy_gemm_f32_gated like the 3xTF32 one.
 #include <cstdio>
 #include <cstdlib>
 #include "lpy_internal.h"
