@@ -68,6 +68,34 @@ def test_gated_ready_flags_bitwise_ungated(path, M, N, K, chunk_k):
 
 
 @pytest.mark.parametrize("path", ["ffma", "3xtf32"])
+@pytest.mark.parametrize("M,N,K,chunk_k", [(4, 4, 40, 32), (1, 8, 64, 32), (128, 4, 96, 32), (200, 300, 48, 4096),
+                                           (257, 132, 4100, 64)])
+def test_gated_edge_shapes(path, M, N, K, chunk_k):
+    """Gate edges: a short last chunk (K = 40 over 32-row chunks), one chunk
+    longer than K, a single-row and a 4-column product (16-byte rows: a gated
+    operand cannot go through the repack), and many small chunks
+    over a K that is not a multiple of the k-block -- the flags are raised one
+    by one from a second stream after a delay; bitwise the ungated product."""
+    A, B = _inputs(M, N, K, seed=17)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    nflags = -(-K // chunk_k)
+    flags = torch.zeros(nflags, dtype=torch.int32, device="cuda")
+    plan = _sms() - 8
+    side = torch.cuda.Stream()
+    torch.cuda._sleep(1)
+    torch.cuda.synchronize()
+    out = lpy.gemm(dA, dB, path=path, opts=_opts(plan), gate=lpy.KGate(flags.data_ptr(), chunk_k, 3, 0))
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(2_000_000)
+        for c in range(nflags):
+            lpy.kgate_signal(flags, c, 3, stream=side)
+    ref = lpy.gemm(dA, dB, path=path, opts=_opts(plan))
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    check(out.cpu().numpy(), A, B)
+
+
+@pytest.mark.parametrize("path", ["ffma", "3xtf32"])
 @pytest.mark.parametrize("la,lb,lc", [(1, 0, 0), (0, 1, 0), (1, 1, 1), (0, 0, 1)])
 def test_gated_layouts_bitwise_ungated(path, la, lb, lc):
     """The gate is on k, which every layout and the column-major-C swap
