@@ -183,7 +183,13 @@ def test_gated_validation_on_device():
     assert lpy.lpy_kgate_signal(flags.data_ptr() + 1, 1, None) == 4
 
 
-_PG = {}
+@pytest.fixture(scope="module", autouse=True)
+def _destroy_world1_group():
+    """Tear down the world-1 NCCL group the row-panel tests create."""
+    yield
+    import torch.distributed as dist
+    if dist.is_initialized():
+        dist.destroy_process_group()
 
 
 def _world1():
