@@ -189,6 +189,8 @@ def _destroy_world1_group():
     yield
     import torch.distributed as dist
     if dist.is_initialized():
+        torch.cuda.synchronize()
+        ldist._state.clear()        # cached communicators / streams of the group being destroyed
         dist.destroy_process_group()
 
 
