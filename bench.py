@@ -316,12 +316,16 @@ def time_path(args, path, rank, world, device, dist_on):
         Bsrc = B.clone()
         clock_hz = 1.9e9
 
+        owned_only = args.bcast == "allgather"    # NVLS all-gather: a rank's SMs move only its own shard
+
         def before_chunk(c, _b=bounds):
             k0, k1 = _b[c]
             nbytes = 4 * (k1 - k0) * B.shape[1]
             wait_s = nbytes / (args.emulate_bcast_gbs * 1e9)
             if wait_s > 2e-6:
                 torch.cuda._sleep(int(wait_s * clock_hz))
+            if owned_only and c % args.emulate_ranks != 0:
+                return          # delivered by the switch: no SM work on this rank
             ctas = max(1, reserve - 1)
             if bulk:
                 rc = probe.lpy_probe_bulk_copy(B[k0:k1].data_ptr(), Bsrc[k0:k1].data_ptr(), nbytes, ctas,
