@@ -46,6 +46,11 @@
 // summed through DSMEM; and an optional K-gate (lpy_gemm_f32_gated) makes the
 // producer wait for each chunk of K to be flagged as arrived before loading it
 // -- the multi-GPU row-panel product consuming B while it is broadcast.
+// Opt-in (LPY_TF32_MC=1, Params::mc): the two CTA pairs of a 4-CTA cluster take
+// vertically adjacent tiles and multicast their shared B boxes (TMA
+// .multicast::cluster), halving B's L2 -> SM traffic; off by default because
+// clusters of 4 leave 16 of 148 SMs unplaced (profiles/r02_tf32_b_multicast.txt).
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include "lpy_internal.h"
@@ -110,7 +115,15 @@ struct Params {
     // `splits` k-slices computed by the `splits` CTA pairs of one cluster, whose
     // partials are summed through distributed shared memory (no ws / sem)
     int cluster_split;
-    float *ws;          // [(num_units - full_tiles)][CG][BM x BN] partial tiles
+    // B multicast (CG = 2, row-major B, BN = 256): clusters of TWO CTA pairs.
+    // Tile t (tiles_m counts pairs of 256-row tiles) is the 512 x BN block
+    // whose pair q in {0, 1} computes 256-row tile 2 tm + q: both pairs need
+    // the same B columns, so CTA (q, r) loads half of its pair-half's B boxes
+    // and multicasts them to CTA (1 - q, r) -- every B byte crosses L2 -> SM
+    // once per cluster instead of once per pair.  A stage is refilled only
+    // after BOTH pairs' MMAs have released it (empty barriers count 2).
+    int mc;
+    float *ws;          // [(num_units - full_tiles)][CG (x2 with mc)][BM x BN] partial tiles
     int *sem;           // 2 x [(num_tiles - full_tiles)][CG] ticket / written counters, zero on entry and exit
     KGate gate;         // operands arriving in chunks of K (lpy_kgate): the producer waits per k-block
 };
@@ -314,7 +327,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int rank = int(crank & 1);
     const uint32_t lead = crank & ~1u;
     const uint16_t pair_mask = uint16_t(3u << lead);
-    const int unit0 = blockIdx.x / CG, units = gridDim.x / CG;   // this pair's first tile, stride
+    // B multicast: pair mq of a 4-CTA cluster; a unit is the cluster's
+    // 512-row block, whose pair mq computes 256-row tile 2 tm + mq (Params::mc)
+    const bool mc = CG == 2 && p.mc;
+    const int mq = mc ? int(crank >> 1) : 0;
+    const int cl = mc ? 2 * CG : CG;                              // CTAs per unit
+    const int unit0 = blockIdx.x / cl, units = gridDim.x / cl;   // this pair's first tile, stride
+    // the operand stages a commit frees: this pair's, or both pairs' (a
+    // multicast writes B into the other pair's stage too)
+    const uint16_t empty_mask = mc ? uint16_t(0xF) : pair_mask;
+    // partial slots of split tiles: one per CTA of the unit
+    const int sub_id = mq * CG + rank, subs = cl;
 
     if (threadIdx.x == 0) {
         TL(0);
@@ -326,7 +349,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&ready[s], CG * XFORM_WARPS);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], mc ? 2 : 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&accf[b], 1);
@@ -361,7 +384,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     int t, kb0, kb1, su, tm, tn;
                     unit_range(u, p, t, kb0, kb1, su);
                     tile_coords(t, p, tm, tn);
-                    const int m0 = tm * (BM * CG) + rank * BM;
+                    const int m0 = (mc ? 2 * tm + mq : tm) * (BM * CG) + rank * BM;
                     const int n0 = tn * BN + rank * C_::BN_CTA;
                     for (int kb = kb0; kb < kb1; ++kb) {
                         // (before the stage wait: off the critical path when the ring is full)
@@ -381,9 +404,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                             tma_load_2d(sa, &tmA, &full[s], k0, m0);
                         }
                         if constexpr (BMN) {
+                            if (mc) {
+                                // this CTA's share of the boxes, to itself and its rank-mate in the other pair
+                                constexpr int PER = C_::BN_CTA / 64;
+                                const uint16_t to = uint16_t((1u << rank) | (1u << (2 + rank)));
 #pragma unroll
-                            for (int j = 0; j < C_::BN_CTA / 32; ++j)
-                                tma_load_2d(sb + j * 2048, &tmB, &full[s], n0 + 32 * j, k0);
+                                for (int j = 0; j < PER; ++j)
+                                    tma_load_2d_mc(sb + (mq * PER + j) * 2048, &tmB, &full[s],
+                                                   n0 + 32 * (mq * PER + j), k0, to);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < C_::BN_CTA / 32; ++j)
+                                    tma_load_2d(sb + j * 2048, &tmB, &full[s], n0 + 32 * j, k0);
+                            }
                         } else {
                             tma_load_2d(sb, &tmB, &full[s], k0, n0);
                         }
@@ -456,7 +489,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 umma_tf32_cg<CG>(d, a_big + SMALL, b_big, idesc, 1u);
                             }
                         }
-                        umma_commit_cg<CG>(&empty[s], pair_mask);
+                        umma_commit_cg<CG>(&empty[s], empty_mask);
                         if (last) umma_commit_cg<CG>(&accf[b], pair_mask);
                         TL(5);
                     }
@@ -590,7 +623,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             auto row_of = [&]() {
                 int tm, tn;
                 tile_coords(t, p, tm, tn);
-                return tm * (BM * CG) + rank * BM + quad * 32 + lane;
+                return (mc ? 2 * tm + mq : tm) * (BM * CG) + rank * BM + quad * 32 + lane;
             };
             auto col0_of = [&]() {
                 int tm, tn;
@@ -627,13 +660,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int me = p.sk_workers > 0
                                    ? su % p.sk_stride - sk_worker_of(static_cast<long long>(vt) * p.k_blocks, p)
                                    : su - vt * p.splits;
-                int *arrive = p.sem + vt * CG + rank;
-                int *written = p.sem + (p.num_tiles - p.full_tiles + vt) * CG + rank;
+                int *arrive = p.sem + vt * subs + sub_id;
+                int *written = p.sem + (p.num_tiles - p.full_tiles + vt) * subs + sub_id;
                 if (ept == 0) last_flag = atomicAdd(arrive, 1) == npieces - 1;
                 named_bar_sync(1, EPI_WARPS * 32);
                 if (!last_flag) {
                     if (ept == 0) TLC(8);
-                    float *mine = p.ws + ((int64_t(su) * CG + rank) * TILE8 + ept) * 8;
+                    float *mine = p.ws + ((int64_t(su) * subs + sub_id) * TILE8 + ept) * 8;
 #pragma unroll
                     for (int j = 0; j < EC; j += 8) st_cg_v8(mine + (j / 8) * 256 * 8, &acc[j]);
                     if (ept == 0) TL(10);
@@ -658,7 +691,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // tile's first or second piece) is written out and the sum
                 // rebuilt from memory in order.
                 auto slot_ptr = [&](int i) {
-                    return p.ws + ((int64_t(split_slot(vt, i, p)) * CG + rank) * TILE8 + ept) * 8;
+                    return p.ws + ((int64_t(split_slot(vt, i, p)) * subs + sub_id) * TILE8 + ept) * 8;
                 };
                 int i0 = 0;
                 if (me >= 2) {
@@ -701,7 +734,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 named_bar_sync(1, EPI_WARPS * 32);
                 int tm, tn;
                 tile_coords(t, p, tm, tn);
-                const int row0 = tm * (BM * CG) + rank * BM, colt = tn * BN;
+                const int row0 = (mc ? 2 * tm + mq : tm) * (BM * CG) + rank * BM, colt = tn * BN;
                 constexpr int C4 = BN / 4;
                 const float *stg = reinterpret_cast<const float *>(stages);
 #pragma unroll 4
@@ -811,7 +844,7 @@ static cudaError_t launch_t(const CUtensorMap &ta, const CUtensorMap &tb, const 
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG * (prm.cluster_split ? prm.splits : 1);
+    attr[0].val.clusterDim.x = CG * (prm.cluster_split ? prm.splits : prm.mc ? 2 : 1);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -967,8 +1000,29 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, const ClusterCap
     prm.c_vec8 = ((reinterpret_cast<uintptr_t>(p.C) & 31) == 0) && (p.ldc % 8 == 0);
     prm.trace = g_trace;
     prm.gate = kn.gate;
+    // B multicast across the two pairs of a 4-CTA cluster (Params::mc):
+    // full-width tiles of a row-major B, an even number of 256-row tiles, and
+    // a schedule of >= 2 waves of clusters (a single under-filled wave takes
+    // the cluster split instead).  LPY_TF32_MC=0 / 1 forces it off / on.
+#ifndef LPY_TF32_MC_DEFAULT
+#define LPY_TF32_MC_DEFAULT 0
+#endif
+    static const int mc_env = [] {
+        const char *e = getenv("LPY_TF32_MC");
+        return e ? atoi(e) : LPY_TF32_MC_DEFAULT;
+    }();
+    const int clusters = std::min(kn.num_sms / (2 * CG), caps.max4);
+    bool mc = CG == 2 && BN == 256 && BMN && mc_env == 1 && prm.tiles_m % 2 == 0 && clusters > 0 &&
+              prm.num_tiles / 2 >= 2 * clusters;
+    if (mc) {
+        prm.mc = 1;
+        prm.tiles_m /= 2;
+        prm.num_tiles = prm.tiles_m * prm.tiles_n;
+        prm.group = std::max(1, prm.group / 2);
+    }
+    const int subs = mc ? 2 * CG : CG;   // CTAs per unit
     {
-        const TailSplit ts = tail_split(prm.num_tiles, prm.k_blocks, kn.num_sms / CG, caps);
+        const TailSplit ts = tail_split(prm.num_tiles, prm.k_blocks, mc ? clusters : kn.num_sms / CG, caps);
         prm.splits = ts.splits;
         prm.full_tiles = ts.full_tiles;
         prm.num_units = ts.num_units;
@@ -983,7 +1037,8 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, const ClusterCap
     }
     prm.ws = nullptr;
     prm.sem = nullptr;
-    int units = (kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms) / CG;  // CTAs (pairs) in the grid
+    int units = (kn.num_ctas > 0 ? kn.num_ctas : kn.num_sms) / subs;  // pairs (clusters with mc) in the grid
+    if (mc && units > clusters) units = clusters;
     if (units > prm.num_units) units = prm.num_units;
     if (units < 1) units = 1;
     // cluster split: one cluster per tile, every pair runs exactly one unit.
@@ -994,17 +1049,17 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, const ClusterCap
         if (kn.num_ctas > 0 && kn.num_ctas / CG < prm.num_units) prm.cluster_split = 0;
         else units = prm.num_units;
     }
-    const int grid = units * CG;
+    const int grid = units * subs;
     if ((prm.splits > 1 && !prm.cluster_split) || prm.sk_workers > 0) {
         const int split_tiles = prm.num_tiles - prm.full_tiles;
         const size_t slots = prm.sk_workers > 0 ? size_t(2) * prm.sk_stride : size_t(split_tiles) * prm.splits;
-        const size_t ws_bytes = slots * CG * BM * BN * 4;
+        const size_t ws_bytes = slots * subs * BM * BN * 4;
         char *buf = nullptr;
-        e = cudaMallocAsync(reinterpret_cast<void **>(&buf), ws_bytes + size_t(split_tiles) * CG * 8, s);
+        e = cudaMallocAsync(reinterpret_cast<void **>(&buf), ws_bytes + size_t(split_tiles) * subs * 8, s);
         if (e != cudaSuccess) return e;
         prm.ws = reinterpret_cast<float *>(buf);
         prm.sem = reinterpret_cast<int *>(buf + ws_bytes);
-        e = cudaMemsetAsync(prm.sem, 0, size_t(split_tiles) * CG * 8, s);
+        e = cudaMemsetAsync(prm.sem, 0, size_t(split_tiles) * subs * 8, s);
         if (e != cudaSuccess) { cudaFreeAsync(buf, s); return e; }
     }
 

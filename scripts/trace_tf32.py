@@ -91,7 +91,7 @@ if ce[0, 0] > 0:
     if sk.any():
         s1 = (ce4[sk, 6] - t0) / 1e3
         print(f"  first split piece's first MMA (leaders) min/med/max {s1.min():.2f}/{s1.median():.2f}/{s1.max():.2f}")
-t = buf[: sms * 8].view(sms, 8).double()
+t = buf[: grid * 8].view(grid, 8).double()
 lead = t[t[:, 0] > 0]
 names = ["mma_total", "mma_wait_ready", "mma_wait_acce", "prod_wait_empty", "xform_wait_full",
          "epi_wait_accf", "xform_busy", "epi_busy"]

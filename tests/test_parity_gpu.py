@@ -547,3 +547,48 @@ def test_stream_k_tail(M, N, K, la, lb):
     for _ in range(3):                                    # repeatable (race detector)
         C, _ = run_gemm(A, B, la=la, lb=lb, path="3xtf32")
         assert np.array_equal(C, ref)
+
+
+MC_CHILD = """
+import sys, torch
+sys.path.insert(0, {root!r})
+import paper_1405_7470_b200 as lpy
+M, N, K = (int(x) for x in sys.argv[1:4])
+g = torch.Generator(device="cuda")
+g.manual_seed(M + N + K)
+A = torch.rand(M, K, device="cuda", generator=g) * 2 - 1
+B = torch.rand(K, N, device="cuda", generator=g) * 2 - 1
+C = lpy.gemm(A, B, path="3xtf32")
+torch.cuda.synchronize()
+torch.save(C.cpu(), sys.argv[4])
+"""
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 4096, 1024), (3000, 5000, 1000), (4096, 4096, 4096)])
+def test_b_multicast_cluster_mode(M, N, K, tmp_path):
+    """B multicast across the two CTA pairs of a 4-CTA cluster (LPY_TF32_MC=1,
+    gemm_3xtf32.cu Params::mc; SURVEY 8(f)-3's cluster TMA multicast): the same
+    MMAs and promotions per tile, so the product is bitwise the default
+    schedule's where neither cuts tiles along k (K < 4096), and within the
+    bound of a float64 reference everywhere (K = 4096 runs stream-K over
+    clusters instead of pairs: different tail pieces)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mc in ("0", "1"):
+        f = tmp_path / f"c{mc}.pt"
+        r = subprocess.run([sys.executable, "-c", MC_CHILD.format(root=root), str(M), str(N), str(K), str(f)],
+                           env={**os.environ, "LPY_TF32_MC": mc}, capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[mc] = torch.load(f)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(M + N + K)
+    A = torch.rand(M, K, device="cuda", generator=g) * 2 - 1
+    B = torch.rand(K, N, device="cuda", generator=g) * 2 - 1
+    ref = (A.double() @ B.double()).cpu()
+    D = (A.abs().double() @ B.abs().double()).cpu()
+    assert ((out["1"].double() - ref).abs() / D).max().item() <= TOL
+    if K < 4096:
+        assert torch.equal(out["0"], out["1"])
