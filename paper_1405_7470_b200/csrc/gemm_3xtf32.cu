@@ -1012,7 +1012,7 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, const ClusterCap
         return e ? atoi(e) : LPY_TF32_MC_DEFAULT;
     }();
     const int clusters = std::min(kn.num_sms / (2 * CG), caps.max4);
-    bool mc = CG == 2 && BN == 256 && BMN && mc_env == 1 && prm.tiles_m % 2 == 0 && clusters > 0 &&
+    bool mc = CG == 2 && BN == 256 && BMN && mc_env == 1 && kn.num_ctas == 0 && prm.tiles_m % 2 == 0 && clusters > 0 &&
               prm.num_tiles / 2 >= 2 * clusters;
     if (mc) {
         prm.mc = 1;
