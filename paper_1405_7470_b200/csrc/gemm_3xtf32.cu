@@ -60,7 +60,6 @@ namespace lpy {
 namespace tf32 {
 
 constexpr int MAX_SPLITS = 4;                // k-slices per split tile (cluster split)
-constexpr int MAX_PIECES = 5;                // pieces of a split tile: stream-K <= SK_MAX_PIECES + 1
 constexpr int BM = 128, BK = 16;             // BM rows per CTA (the tile's BN columns: template, 128/192/256)
 constexpr int THREADS = 512;                 // 16 warps = 4 warpgroups
 constexpr int XFORM_WARP0 = 4, XFORM_WARPS = 4;

@@ -1,0 +1,17 @@
+#!/usr/bin/env python
+"""Cycles per kind::tf32 MMA (K=8) by tile width N, single CTA (M=128) and CTA pair (M=256), A K-major,
+B K- or MN-major (liblpy_probe.so lpy_probe_umma_rate_fmt; full rate = N/2 cycles)."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+P = ctypes.CDLL(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1405_7470_b200", "liblpy_probe.so"))
+P.lpy_probe_umma_rate_fmt.argtypes = [ctypes.c_int] * 6 + [ctypes.c_void_p, ctypes.c_void_p]
+cyc = torch.zeros(1, dtype=torch.int64, device="cuda")
+iters = 4000
+for cg in (1, 2):
+    for fb in (0, 1):
+        for n in (64, 128, 160, 192, 224, 256):
+            rc = P.lpy_probe_umma_rate_fmt(n, 0, fb, iters, 148, cg, cyc.data_ptr(), None)
+            torch.cuda.synchronize()
+            c = cyc.item() / iters
+            print(f"cg={cg} fb={fb} N={n:3d}: {c:7.2f} cycles/MMA  ({n / 2 / c:.2f} of full rate)  rc={rc}", flush=True)
