@@ -159,6 +159,16 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- CPU oracle
+def host_cores() -> int:
+    """The host cores this process may run on.  The oracle is timed on all of
+    them: torchrun sets OMP_NUM_THREADS=1 for every rank, but at N > 1 only
+    rank 0 runs the oracle while the others wait."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except (AttributeError, OSError):
+        return max(1, os.cpu_count() or 1)
+
+
 def oracle_sample(n: int, seconds: float, dist_name: str, nthreads: int = 0):
     """Time the float64 oracle on a bounded sample of the n x n x n product:
     the first R rows of C (R sized to ~`seconds`).  Returns (GFLOP/s, sample
@@ -219,7 +229,7 @@ def run_reference(args, rank, world):
     # --ref-total seconds (a few minutes at most), at least 0.2 s of work per step
     per_step = max(0.2, min(args.ref_seconds, args.ref_total / max(1, args.steps + args.warmup)))
     # calibrate the sample once, then time each step on that fixed sample
-    gf, dt, sample, threads = oracle_sample(n, per_step, "uniform")
+    gf, dt, sample, threads = oracle_sample(n, per_step, "uniform", nthreads=host_cores())
     times = []
     import numpy as np
     import synth
@@ -808,7 +818,7 @@ def main():
         cpu = None
         if not args.no_cpu:
             # rank 0's host cores at every N (the other ranks wait at the final barrier)
-            gf, dt, sample, threads = oracle_sample(n, args.cpu_seconds, "uniform")
+            gf, dt, sample, threads = oracle_sample(n, args.cpu_seconds, "uniform", nthreads=host_cores())
             cpu = {"value": round(gf, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
                    "sample": sample, "seconds": round(dt, 2), "cpu_model": cpu_model()}
         line = {
