@@ -519,3 +519,115 @@ extern "C" int lpy_probe_bulk_copy(void *dst, const void *src, long long bytes, 
         static_cast<char *>(dst), static_cast<const char *>(src), bytes);
     return int(cudaGetLastError());
 }
+
+// ---------------------------------------------------------------- MMA rate with commits
+// As umma_rate_fmt_kernel (A K-major 64B-swizzled format 2, B MN-major format 3),
+// plus a tcgen05.commit to one of 8 rotating mbarriers after every `every`
+// groups of six MMAs (0: none), and optionally (`wait` != 0) the issuing thread waiting for each
+// commit `lag` commits later -- the 3xTF32 kernel's per-k-block pattern
+// (six MMAs, a commit freeing the stage).  Does a commit cost the pipe?
+namespace lpy {
+namespace probe {
+template <int CG>
+__global__ void umma_rate_commit_kernel(int N, int iters, int every, int lag, long long *cycles) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t *base = smem_raw + (((raw + 1023) & ~1023u) - raw);
+    __shared__ uint64_t bars[8];
+    __shared__ uint64_t done;              // completed once, before the loop
+    __shared__ uint32_t tmem_base;
+    const int nb = N / CG;
+    for (int i = threadIdx.x; i < (128 + nb) * 32; i += blockDim.x)
+        reinterpret_cast<float *>(base)[i] = 1.0f;
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
+        mbar_init(&done, 1);
+        fence_mbar_init();
+        mbar_arrive(&done);
+    }
+    if (threadIdx.x < 32) {
+        tmem_alloc_cg<CG>(&tmem_base, 256);
+        tmem_relinquish_cg<CG>();
+    }
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    if (threadIdx.x < 32 && rank == 0) {
+        // the whole warp runs the loop converged (descriptors in uniform registers), one
+        // elected lane issues -- as the 3xTF32 kernel's MMA warp does; 6 MMAs per "k-block"
+        const uint32_t idesc = umma_idesc_tf32(128 * CG, N, 0, 1);
+        const uint32_t sa = smem_u32(base), sb = smem_u32(base) + 128 * 128;
+        const uint64_t a0 = desc(2, sa, 0, 128), a1 = desc(2, sa, 1, 128);
+        const uint64_t b0 = desc(3, sb, 0, nb), b1 = desc(3, sb, 1, nb);
+        const int kblocks = iters / 6;
+        long long t0 = clock64();
+        for (int kb = 0; kb < kblocks; ++kb) {
+            if (elect_one()) {
+                umma_tf32_cg<CG>(tmem_base, a0, b0, idesc, kb > 0 ? 1u : 0u);
+                umma_tf32_cg<CG>(tmem_base, a0, b1, idesc, 1u);
+                umma_tf32_cg<CG>(tmem_base, a1, b0, idesc, 1u);
+                umma_tf32_cg<CG>(tmem_base, a1, b1, idesc, 1u);
+                umma_tf32_cg<CG>(tmem_base, a0, b0, idesc, 1u);
+                umma_tf32_cg<CG>(tmem_base, a1, b1, idesc, 1u);
+                if (every > 0 && (kb + 1) % every == 0) umma_commit_cg<CG>(&bars[(kb / every) & 7]);
+            }
+            __syncwarp();
+            // mode (lag < 0): -1 fence only, -2 wait on an always-complete barrier + fence,
+            // -3 that wait without the fence; lag in 1..7: wait on the commit `lag` back + fence,
+            // lag in 9..15: the same wait (lag - 8 back) without the fence
+            if (lag == -1) {
+                tc_fence_after();
+            } else if (lag == -2 || lag == -3) {
+                mbar_wait(&done, 0);
+                if (lag == -2) tc_fence_after();
+            } else if (every > 0 && lag > 0 && (kb + 1) % every == 0 && kb / every >= (lag & 7)) {
+                const int w = kb / every - (lag & 7);
+                mbar_wait(&bars[w & 7], uint32_t((w >> 3) & 1));
+                if (lag < 8) tc_fence_after();
+            }
+        }
+        __shared__ uint64_t fin;
+        if (elect_one()) {
+            mbar_init(&fin, 1);
+            fence_mbar_init();
+            umma_commit_cg<CG>(&fin);
+        }
+        __syncwarp();
+        mbar_wait(&fin, 0);
+        long long t1 = clock64();
+        if (blockIdx.x == 0 && threadIdx.x == 0) *cycles = t1 - t0;
+    }
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    if (threadIdx.x < 32) tmem_dealloc_cg<CG>(tmem_base, 256);
+}
+}  // namespace probe
+}  // namespace lpy
+
+extern "C" int lpy_probe_umma_rate_commit(int N, int iters, int every, int lag, int ctas, int cg,
+                                          long long *cycles_dev, void *stream) {
+    const size_t smem = 1024 + size_t(128 + 256) * 32 * 4;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cg;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cg == 2) {
+        cudaFuncSetAttribute(lpy::probe::umma_rate_commit_kernel<2>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        return int(cudaLaunchKernelEx(&cfg, lpy::probe::umma_rate_commit_kernel<2>, N, iters, every, lag,
+                                      cycles_dev));
+    }
+    cudaFuncSetAttribute(lpy::probe::umma_rate_commit_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    return int(cudaLaunchKernelEx(&cfg, lpy::probe::umma_rate_commit_kernel<1>, N, iters, every, lag, cycles_dev));
+}

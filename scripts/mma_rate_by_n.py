@@ -8,10 +8,22 @@ P = ctypes.CDLL(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__f
 P.lpy_probe_umma_rate_fmt.argtypes = [ctypes.c_int] * 6 + [ctypes.c_void_p, ctypes.c_void_p]
 cyc = torch.zeros(1, dtype=torch.int64, device="cuda")
 iters = 4000
-for cg in (1, 2):
-    for fb in (0, 1):
-        for n in (64, 128, 160, 192, 224, 256):
+for cg in (2,):
+    for fb in (1,):
+        for n in (128, 256):
             rc = P.lpy_probe_umma_rate_fmt(n, 0, fb, iters, 148, cg, cyc.data_ptr(), None)
             torch.cuda.synchronize()
             c = cyc.item() / iters
             print(f"cg={cg} fb={fb} N={n:3d}: {c:7.2f} cycles/MMA  ({n / 2 / c:.2f} of full rate)  rc={rc}", flush=True)
+
+# commits after every `every` k-blocks of 6 MMAs (the 3xTF32 k-block), the issuer waiting on the commit `lag` commits back
+P.lpy_probe_umma_rate_commit.argtypes = [ctypes.c_int] * 6 + [ctypes.c_void_p, ctypes.c_void_p]
+iters = 6000
+for cg in (1, 2):
+    for n in (128, 256):
+        for every, lag in ((0, 0), (1, 0), (1, 2), (1, 4), (1, 10), (1, 12), (0, -1), (0, -2), (0, -3), (2, 2)):
+            rc = P.lpy_probe_umma_rate_commit(n, iters, every, lag, 148, cg, cyc.data_ptr(), None)
+            torch.cuda.synchronize()
+            c = cyc.item() / iters
+            print(f"commit cg={cg} N={n:3d} every={every:2d} lag={lag}: {c:7.2f} cycles/MMA ({n / 2 / c:.2f} of full)  rc={rc}",
+                  flush=True)
