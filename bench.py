@@ -322,7 +322,12 @@ def time_path(args, path, rank, world, device, dist_on):
                                                     ctypes.c_int, ctypes.c_void_p]
         probe.lpy_probe_bulk_copy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int,
                                               ctypes.c_void_p]
-        bulk = os.environ.get("LPY_EMUL_COPY", "threads") == "bulk"   # TMA bulk copies instead of thread copies
+        copy_mode = os.environ.get("LPY_EMUL_COPY", "threads")
+        bulk = copy_mode == "bulk"        # TMA bulk copies instead of thread copies
+        # cudaMemcpyAsync pulls (a dist copy-engine pull mode's stand-in) -- but on one GPU the
+        # device-to-device copies ran on SMs (profiles/r02_ce_emul.txt), so this does not model
+        # NVLink copy-engine pulls
+        ce = copy_mode == "ce"
         Bsrc = B.clone()
         clock_hz = 1.9e9
 
@@ -334,6 +339,12 @@ def time_path(args, path, rank, world, device, dist_on):
             wait_s = nbytes / (args.emulate_bcast_gbs * 1e9)
             if wait_s > 2e-6:
                 torch.cuda._sleep(int(wait_s * clock_hz))
+            if ce:
+                # the rank pulls every chunk it does not own from its owner with its copy
+                # engines (dist "ce" mode: each chunk c is owned by rank c mod g)
+                if c % args.emulate_ranks != 0:
+                    B[k0:k1].copy_(Bsrc[k0:k1], non_blocking=True)
+                return
             if owned_only and c % args.emulate_ranks != 0:
                 return          # delivered by the switch: no SM work on this rank
             ctas = max(1, reserve - 1)
