@@ -896,7 +896,13 @@ cudaError_t launch_ffma(const Problem &p, const Knobs &kn, cudaStream_t s) {
         const int64_t waves = (tiles + grid - 1) / grid;
         return kern * double(tiles) / double(waves * grid) * double(p.N) / double(((p.N + bn - 1) / bn) * bn);
     };
-    if (kn.tile_n == 256 || (kn.tile_n == 0 && eff(256, 1.04) >= eff(128, 1.0))) {
+    // The 4% per-flop edge of 256 shows only on long k loops: with K <= 2048 (<= 64
+    // k-blocks per tile) 128-wide tiles -- half the partial bytes per split and
+    // twice the units to balance -- measured 2-5% faster where the wave fill ties
+    // (config 5 115 -> 110 us, n=2048 310 -> 304 us, 1536x2048x2048 240 -> 233 us;
+    // 2048x2048x8192 and 1024x8192x8192 keep 256: profiles/r02_ffma_tile_width.txt).
+    const double kern256 = p.K >= 4096 ? 1.04 : 0.98;
+    if (kn.tile_n == 256 || (kn.tile_n == 0 && eff(256, kern256) >= eff(128, 1.0))) {
         if (AK && BKM)  return launch_t<true, true, 256>(p, kn, s);
         if (AK && !BKM) return launch_t<true, false, 256>(p, kn, s);
         if (!AK && BKM) return launch_t<false, true, 256>(p, kn, s);
