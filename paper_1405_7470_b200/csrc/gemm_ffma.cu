@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(CWARPS * 32) splitk_fixup_kernel(const Params 
 // Stream-K for a ragged or under-filled last wave (the paper's "separate code
 // for edge and corner cases", as a fractional split): tiles
 // [0, (waves - 1) P) run whole, the last wave's rem tiles are dealt out as
-// rem * k_blocks k-block iterations over P' = min(P, iterations / 4) workers,
+// rem * k_blocks k-block iterations over P' = min(P, iterations / 12) workers,
 // so it lasts rem / P' of a tile instead of a whole one.  Taken when its
 // modelled length -- the fix-up costs the last piece of a tile the reads of
 // the others' 128 KB partials and every other piece one write, ~2.6 us each
@@ -656,7 +656,10 @@ static StreamK choose_stream_k(int tiles, int k_blocks, int P, int splits, int b
     if (rem == P) return r;
     const long long iters = static_cast<long long>(rem) * k_blocks;
     long long workers = P;
-    if (workers > iters / 4) workers = iters / 4;             // >= 4 k-blocks per worker
+    // >= 12 k-blocks per worker: shorter pieces lose to split-K -- config 5 at
+    // BN = 128 (7.4 k-blocks per worker) ran 110 us stream-K'd vs 107 us split
+    // (profiles/r02_ffma_schedule.txt); n = 2048 (47 per worker) 304 vs 312
+    if (workers > iters / 12) workers = iters / 12;
     if (workers <= rem) return r;
     const double kb_us = bn == 256 ? 4.2 : 2.1;               // one k-block of one tile at full FMA rate
     const double tile_us = k_blocks * kb_us;
