@@ -919,7 +919,11 @@ static TailSplit tail_split(int num_tiles, int k_blocks, int pairs, const Cluste
     // SM while the pair's TMA traffic shares the port (~5 us per partial,
     // scripts/trace_tf32.py, profiles/r02_streamk.txt) -- at K = 1024 (64
     // k-blocks, ~34 us per tile) that ate the whole gain.
-    if (!streamk || rem == pairs || k_blocks < SK_MIN_TILE_KB) return r;
+    static const int min_tile_kb = [] {    // LPY_TF32_SK_MINKB (A/B): shortest k loop worth stream-K
+        const char *e = getenv("LPY_TF32_SK_MINKB");
+        return e ? atoi(e) : SK_MIN_TILE_KB;
+    }();
+    if (!streamk || rem == pairs || k_blocks < min_tile_kb) return r;
     static const int force_workers = [] {   // LPY_TF32_SKW=n: n stream-K workers (diagnostics / A-B)
         const char *e = getenv("LPY_TF32_SKW");
         return e ? atoi(e) : 0;
