@@ -711,6 +711,12 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
         return e ? atoi(e) : 1;
     }();
     prm.splits = choose_splits(prm.num_tiles, prm.k_blocks, kn.num_sms, min_kb, MAX_SPLITS);
+    static const int force_splits = [] {   // LPY_FFMA_SPLITS=S (A/B): split-K factor, 0 = choose_splits
+        const char *e = getenv("LPY_FFMA_SPLITS");
+        const int v = e ? atoi(e) : 0;
+        return v >= 1 && v <= MAX_SPLITS ? v : 0;
+    }();
+    if (force_splits) prm.splits = force_splits;
     prm.num_units = prm.num_tiles * prm.splits;
     prm.ws = nullptr;
     prm.sem = nullptr;
