@@ -576,6 +576,10 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
             }
         }
     }
+    // the split-K fix-up (launched with programmatic dependent launch) may start
+    // once every CTA's consumers are past their last unit; it waits for this
+    // grid's completion (griddepcontrol.wait) before reading the partials
+    if constexpr (SPLIT) pdl_launch_dependents();
 }
 
 // Split-K fix-up: FIXUP_PARTS CTAs of 256 threads per output tile, part r
@@ -588,6 +592,7 @@ __global__ void __launch_bounds__(Geo<AK, BKM, BN, SPLIT>::THREADS, 1)
 constexpr int FIXUP_PARTS = 8;   // 8 vs 4: ragged config 103.3 -> 102.5 us, others equal (profiles/r01_ffma_partial_layout.txt)
 template <int BN>
 __global__ void __launch_bounds__(CWARPS * 32) splitk_fixup_kernel(const Params p) {
+    pdl_wait();                 // the slices' partials (the split-K grid) are complete and visible
     constexpr int JN = BN / 32;
     const int IPART = 8 / int(gridDim.y);   // gridDim.y = parts per tile (1, 2, 4 or 8)
     const int t = blockIdx.x;
@@ -863,7 +868,7 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
         cfg.blockDim = dim3(CWARPS * 32);
         cfg.stream = s;
         cfg.attrs = attr;
-        cfg.numAttrs = 0;
+        cfg.numAttrs = pdl_attr(attr, 0);   // its launch overlaps the split grid's tail
         e = cudaLaunchKernelEx(&cfg, splitk_fixup_kernel<BN>, prm);
     }
     if (prm.ws) cudaFreeAsync(prm.ws, s);
