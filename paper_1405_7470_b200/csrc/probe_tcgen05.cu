@@ -529,7 +529,7 @@ extern "C" int lpy_probe_bulk_copy(void *dst, const void *src, long long bytes, 
 namespace lpy {
 namespace probe {
 template <int CG>
-__global__ void umma_rate_commit_kernel(int N, int iters, int every, int lag, long long *cycles) {
+__global__ void umma_rate_commit_kernel(int N, int iters, int every, int lag, int pattern, long long *cycles) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t *base = smem_raw + (((raw + 1023) & ~1023u) - raw);
@@ -547,7 +547,7 @@ __global__ void umma_rate_commit_kernel(int N, int iters, int every, int lag, lo
         mbar_arrive(&done);
     }
     if (threadIdx.x < 32) {
-        tmem_alloc_cg<CG>(&tmem_base, 256);
+        tmem_alloc_cg<CG>(&tmem_base, 512);
         tmem_relinquish_cg<CG>();
     }
     tc_fence_before();
@@ -565,12 +565,26 @@ __global__ void umma_rate_commit_kernel(int N, int iters, int every, int lag, lo
         long long t0 = clock64();
         for (int kb = 0; kb < kblocks; ++kb) {
             if (elect_one()) {
+                if (CG == 2 && pattern > 0) {
+                    // the 3xTF32 kernel's k-block: per k-slice of 8, A_big x B_small and A_big x B_big
+                    // through the A collector (fill / lastuse), then A_small x B_big from shared
+                    // memory (pattern 1) or from TMEM columns 256.. (pattern 2, the TS form)
+#pragma unroll
+                    for (int sub = 0; sub < 2; ++sub) {
+                        const uint64_t a = sub ? a1 : a0, b = sub ? b1 : b0, bs = sub ? b0 : b1;
+                        umma_tf32_cg2_coll<ACollector::Fill>(tmem_base, a, bs, idesc, (kb > 0 || sub) ? 1u : 0u);
+                        umma_tf32_cg2_coll<ACollector::LastUse>(tmem_base, a, b, idesc, 1u);
+                        if (pattern == 2) umma_tf32_ts_cg2(tmem_base, tmem_base + 256 + 8 * sub, b, idesc, 1u);
+                        else              umma_tf32_cg<CG>(tmem_base, sub ? a0 : a1, b, idesc, 1u);
+                    }
+                } else {
                 umma_tf32_cg<CG>(tmem_base, a0, b0, idesc, kb > 0 ? 1u : 0u);
                 umma_tf32_cg<CG>(tmem_base, a0, b1, idesc, 1u);
                 umma_tf32_cg<CG>(tmem_base, a1, b0, idesc, 1u);
                 umma_tf32_cg<CG>(tmem_base, a1, b1, idesc, 1u);
                 umma_tf32_cg<CG>(tmem_base, a0, b0, idesc, 1u);
                 umma_tf32_cg<CG>(tmem_base, a1, b1, idesc, 1u);
+                }
                 if (every > 0 && (kb + 1) % every == 0) umma_commit_cg<CG>(&bars[(kb / every) & 7]);
             }
             __syncwarp();
@@ -601,12 +615,12 @@ __global__ void umma_rate_commit_kernel(int N, int iters, int every, int lag, lo
     }
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
-    if (threadIdx.x < 32) tmem_dealloc_cg<CG>(tmem_base, 256);
+    if (threadIdx.x < 32) tmem_dealloc_cg<CG>(tmem_base, 512);
 }
 }  // namespace probe
 }  // namespace lpy
 
-extern "C" int lpy_probe_umma_rate_commit(int N, int iters, int every, int lag, int ctas, int cg,
+extern "C" int lpy_probe_umma_rate_commit(int N, int iters, int every, int lag, int pattern, int ctas, int cg,
                                           long long *cycles_dev, void *stream) {
     const size_t smem = 1024 + size_t(128 + 256) * 32 * 4;
     cudaLaunchConfig_t cfg = {};
@@ -624,10 +638,11 @@ extern "C" int lpy_probe_umma_rate_commit(int N, int iters, int every, int lag, 
     if (cg == 2) {
         cudaFuncSetAttribute(lpy::probe::umma_rate_commit_kernel<2>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        return int(cudaLaunchKernelEx(&cfg, lpy::probe::umma_rate_commit_kernel<2>, N, iters, every, lag,
+        return int(cudaLaunchKernelEx(&cfg, lpy::probe::umma_rate_commit_kernel<2>, N, iters, every, lag, pattern,
                                       cycles_dev));
     }
     cudaFuncSetAttribute(lpy::probe::umma_rate_commit_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem));
-    return int(cudaLaunchKernelEx(&cfg, lpy::probe::umma_rate_commit_kernel<1>, N, iters, every, lag, cycles_dev));
+    return int(cudaLaunchKernelEx(&cfg, lpy::probe::umma_rate_commit_kernel<1>, N, iters, every, lag, pattern,
+                                  cycles_dev));
 }

@@ -16,14 +16,16 @@ for cg in (2,):
             c = cyc.item() / iters
             print(f"cg={cg} fb={fb} N={n:3d}: {c:7.2f} cycles/MMA  ({n / 2 / c:.2f} of full rate)  rc={rc}", flush=True)
 
-# commits after every `every` k-blocks of 6 MMAs (the 3xTF32 k-block), the issuer waiting on the commit `lag` commits back
-P.lpy_probe_umma_rate_commit.argtypes = [ctypes.c_int] * 6 + [ctypes.c_void_p, ctypes.c_void_p]
+# commits after every `every` k-blocks of 6 MMAs (the 3xTF32 k-block), the issuer waiting on the commit `lag` commits
+# back; pattern 0: six plain SS MMAs, 1: the kernel's (collector fill / lastuse + SS), 2: the same with the third MMA
+# in TS form (A from TMEM)
+P.lpy_probe_umma_rate_commit.argtypes = [ctypes.c_int] * 7 + [ctypes.c_void_p, ctypes.c_void_p]
 iters = 6000
-for cg in (1, 2):
-    for n in (128, 256):
-        for every, lag in ((0, 0), (1, 0), (1, 2), (1, 4), (1, 10), (1, 12), (0, -1), (0, -2), (0, -3), (2, 2)):
-            rc = P.lpy_probe_umma_rate_commit(n, iters, every, lag, 148, cg, cyc.data_ptr(), None)
+for pattern in (0, 1, 2):
+    for n in (128, 192, 256):
+        for every, lag in ((0, 0), (1, 0), (0, -2)):
+            rc = P.lpy_probe_umma_rate_commit(n, iters, every, lag, pattern, 148, 2, cyc.data_ptr(), None)
             torch.cuda.synchronize()
             c = cyc.item() / iters
-            print(f"commit cg={cg} N={n:3d} every={every:2d} lag={lag}: {c:7.2f} cycles/MMA ({n / 2 / c:.2f} of full)  rc={rc}",
+            print(f"pattern={pattern} cg=2 N={n:3d} every={every} lag={lag:2d}: {c:7.2f} cycles/MMA ({n / 2 / c:.2f} of full)  rc={rc}",
                   flush=True)
