@@ -36,7 +36,8 @@
 //                ragged K).
 // Operand smem layouts: K-major tiles use the 64B swizzle (16 fp32 per row);
 // MN-major tf32 tiles must use SWIZZLE_128B_BASE32B (TMA "128B_ATOM_32B").
-// Narrow tiles (BN <= 192) with a K-major A keep A_small in TENSOR memory: the
+// Tile widths 128 / 176 / 192 / 256 (176 only for K-major A and B: config 5 fills 72 of
+// 74 pairs).  Narrow tiles (BN <= 192) with a K-major A keep A_small in TENSOR memory: the
 // transform warps write each row's 16 small values with tcgen05.st and the
 // a_small * b_big MMA reads A from TMEM (TS form), so that tile never crosses
 // the shared-memory port.
@@ -540,8 +541,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                     tmem_st_x16(tmem + (uint32_t((xt >> 5) * 32) << 16) + uint32_t(2 * BN + 16 * s), v);
                     // B: as below, over the B part of the stage only
                     constexpr int A4 = int(A_BYTES / 16), B_PER = int(C_::B_BYTES / 16) / (XFORM_WARPS * 32);
+                    constexpr int B_REM = int(C_::B_BYTES / 16) % (XFORM_WARPS * 32);   // (BN = 176: 96)
 #pragma unroll 4
-                    for (int i = 0; i < B_PER; ++i) {
+                    for (int i = 0; i < B_PER + (B_REM ? 1 : 0); ++i) {
+                        if (B_REM && i == B_PER && xt >= B_REM) break;
                         float4 w = src[A4 + xt + i * XFORM_WARPS * 32];
                         w.x = tf32_small(w.x);
                         w.y = tf32_small(w.y);
@@ -598,7 +601,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tc_fence_after();
                 const uint32_t base = tmem + lane_base + b * acc_stride + half * EC;
 #pragma unroll
-                for (int c = 0; c < EC; c += 32) {
+                for (int c = 0; c + 32 <= EC; c += 32) {
                     uint32_t v0[16], v1[16];
                     tmem_ld_x16(base + c, v0);
                     tmem_ld_x16(base + c + 16, v1);
@@ -608,6 +611,22 @@ __global__ void __launch_bounds__(THREADS, 1)
                         acc[c + j] += __uint_as_float(v0[j]);
                         acc[c + 16 + j] += __uint_as_float(v1[j]);
                     }
+                }
+                if constexpr (EC % 32 >= 16) {            // (BN = 176: columns 64..79 of 88)
+                    constexpr int c = EC / 32 * 32;
+                    uint32_t v0[16];
+                    tmem_ld_x16(base + c, v0);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) acc[c + j] += __uint_as_float(v0[j]);
+                }
+                if constexpr (EC % 16 == 8) {             // (BN = 176: columns 80..87)
+                    constexpr int c = EC - 8;
+                    uint32_t v0[8];
+                    tmem_ld_x8(base + c, v0);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[c + j] += __uint_as_float(v0[j]);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -832,7 +851,9 @@ template <int CG, bool AMN, bool BMN, int BN>
 static cudaError_t launch_t(const CUtensorMap &ta, const CUtensorMap &tb, const Params &prm, int grid,
                             cudaStream_t s) {
     using C_ = Cfg<CG, BN>;
-    static_assert(C_::EC % 32 == 0 && C_::SMEM_BYTES <= 227 * 1024, "tile does not fit");
+    static_assert(C_::EC % 8 == 0 && C_::SMEM_BYTES <= 227 * 1024, "tile does not fit");
+    // 32-column MN-major B boxes, whole float4 shares of the transform outside the TMEM-A path
+    static_assert(BN % 64 == 0 || (!AMN && !BMN), "BN = 176 needs K-major A and B");
     auto kern = gemm_3xtf32_kernel<CG, AMN, BMN, BN>;
     static std::atomic<uint64_t> attr_done{0};
     if (cudaError_t e = ensure_smem_attr(kern, int(C_::SMEM_BYTES), attr_done); e != cudaSuccess) return e;
@@ -960,19 +981,21 @@ static TailSplit tail_split(int num_tiles, int k_blocks, int pairs, const Cluste
 // over the useful columns; narrower wins only by > 3%.  n >= 4096 -> 256;
 // n = 1024 -> 128 (32 tiles instead of 16); the ragged config -> 192 (64 tiles
 // instead of 48).
-int choose_bn(int M, int N, int K, int pairs, const ClusterCaps &caps) {
+int choose_bn(int M, int N, int K, int pairs, const ClusterCaps &caps, bool kmajor_ab) {
     const int64_t tm = (M + 2 * BM - 1) / (2 * BM);
     const int kb = (K + BK - 1) / BK;
     auto cost = [&](int bn) {
         const int64_t tn = (N + bn - 1) / bn, tiles = tm * tn;
         const TailSplit ts = tail_split(int(tiles), kb, pairs, caps);
-        const double kern = bn == 256 ? 1.0 : bn == 192 ? 0.94 : 0.80;
+        const double kern = bn == 256 ? 1.0 : bn == 192 ? 0.94 : bn == 176 ? 0.92 : 0.80;
         return ts.waves * bn / kern * double(tn * bn) / double(N);
     };
     int best = 256;
     double best_cost = cost(256);
-    for (int bn : {192, 128})
+    for (int bn : {192, 176, 128}) {
+        if (bn == 176 && !kmajor_ab) continue;   // 176-wide tiles exist for K-major A and B only
         if (cost(bn) * 1.03 < best_cost) { best = bn; best_cost = cost(bn); }
+    }
     return best;
 }
 
@@ -1067,10 +1090,14 @@ static cudaError_t launch_cg(const Problem &p, const Knobs &kn, const ClusterCap
     }
 
     auto launch = [&](const Params &q, int g) {
-        if (AMN && BMN)  return launch_t<CG, true, true, BN>(ta, tb, q, g, s);
-        if (AMN && !BMN) return launch_t<CG, true, false, BN>(ta, tb, q, g, s);
-        if (!AMN && BMN) return launch_t<CG, false, true, BN>(ta, tb, q, g, s);
-        return launch_t<CG, false, false, BN>(ta, tb, q, g, s);
+        if constexpr (BN % 64 != 0) {   // (176: K-major A and B only, choose_bn's contract)
+            return (AMN || BMN) ? cudaErrorInvalidValue : launch_t<CG, false, false, BN>(ta, tb, q, g, s);
+        } else {
+            if (AMN && BMN)  return launch_t<CG, true, true, BN>(ta, tb, q, g, s);
+            if (AMN && !BMN) return launch_t<CG, true, false, BN>(ta, tb, q, g, s);
+            if (!AMN && BMN) return launch_t<CG, false, true, BN>(ta, tb, q, g, s);
+            return launch_t<CG, false, false, BN>(ta, tb, q, g, s);
+        }
     };
     e = launch(prm, grid);
     if (e != cudaSuccess && prm.cluster_split) {
@@ -1152,9 +1179,12 @@ cudaError_t launch_3xtf32(const Problem &p, const Knobs &kn, cudaStream_t s) {
     // or from opts.tile_n (dist.py's per-chunk products, which share the GPU,
     // ask for full-width tiles)
     const int pairs = kn.num_sms / 2;
-    const int bn = kn.tile_n ? kn.tile_n : force_bn ? force_bn : tf32::choose_bn(p.M, p.N, p.K, pairs > 0 ? pairs : 1, caps);
+    const bool kmajor_ab = p.la == 0 && p.lb == 1;   // row-major A, column-major B
+    const int bn = kn.tile_n ? kn.tile_n : force_bn ? force_bn : tf32::choose_bn(p.M, p.N, p.K, pairs > 0 ? pairs : 1, caps,
+                                                                                kmajor_ab);
     switch (bn) {
         case 128: return tf32::launch_cg<2, 128>(p, kn, caps, s);
+        case 176: return kmajor_ab ? tf32::launch_cg<2, 176>(p, kn, caps, s) : cudaErrorInvalidValue;
         case 192: return tf32::launch_cg<2, 192>(p, kn, caps, s);
         default:  return tf32::launch_cg<2, 256>(p, kn, caps, s);
     }
