@@ -122,7 +122,9 @@ typedef struct lpy_gemm_opts {
                              /* before promotion; 0 = auto (8); 1..16, larger values */
                              /* are LPY_ERR_INVALID_VALUE (32 measured 1.05e-5 on    */
                              /* uniform[0,1) at K = 8192: beyond the contract)       */
-    int32_t tile_n;          /* output-tile width: 0 = auto (from shape and device), */
+    int32_t tile_n;          /* output-tile width: 0 = auto (from shape and device;  */
+                             /* auto may also pick 176 on 3xTF32 for row-major A     */
+                             /* with column-major B, a width not selectable here),   */
                              /* else 128 or 256 (both paths) or 192 (3xTF32 only;    */
                              /* LPY_ERR_NOT_SUPPORTED on FFMA); other values are     */
                              /* LPY_ERR_INVALID_VALUE.  Results do not depend on the  */
