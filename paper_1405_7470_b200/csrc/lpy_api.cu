@@ -451,10 +451,27 @@ lpy_status lpy_gemm_f32_host(int64_t M, int64_t N, int64_t K, const float *A, in
     // panel's product and download are the exposed tail after the upload ends
     const int64_t prow = M <= 1024 ? M
                                    : std::max<int64_t>(512, ((M + kMaxPanels - 1) / kMaxPanels + 127) / 128 * 128);
-    const int npanel = int((M + prow - 1) / prow);
+    // Panel q covers rows [pb[q], pb[q + 1]).  The last regular panel is cut
+    // into halving pieces (L/2, L/4, L/4; multiples of 128): its product and
+    // download are the exposed tail after the last upload, so the tail is
+    // the smallest piece's, not a whole panel's.
+    int64_t pb[kMaxPanels + 3];
+    int npanel = 0;
+    pb[0] = 0;
+    for (int64_t r = 0; r < M; r += prow) {
+        const int64_t len = std::min(prow, M - r);
+        if (r + len == M && M > 1024 && len >= 512) {
+            const int64_t h1 = (len / 2 + 127) / 128 * 128, h2 = ((len - h1) / 2 + 127) / 128 * 128;
+            pb[++npanel] = r + h1;
+            pb[++npanel] = r + h1 + h2;
+            pb[++npanel] = M;
+        } else {
+            pb[++npanel] = r + len;
+        }
+    }
     cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_b = nullptr, ev_done = nullptr;
-    cudaEvent_t ev_a[kMaxPanels] = {}, ev_c[kMaxPanels] = {};
+    cudaEvent_t ev_a[kMaxPanels + 2] = {}, ev_c[kMaxPanels + 2] = {};
     auto mk_stream = [&](cudaStream_t *x) {
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(x, cudaStreamNonBlocking);
     };
@@ -488,13 +505,13 @@ lpy_status lpy_gemm_f32_host(int64_t M, int64_t N, int64_t K, const float *A, in
         e = copy_lines(dev_buf[1], dev_ld[1], ob.p, ob.ld, ob.inner(), ob.lines(), cudaMemcpyHostToDevice, sh);
     if (e == cudaSuccess) e = cudaEventRecord(ev_b, sh);
     for (int q = 0; q < npanel && e == cudaSuccess; ++q) {
-        const int64_t r0 = q * prow, r1 = std::min(M, r0 + prow);
+        const int64_t r0 = pb[q], r1 = pb[q + 1];
         e = copy_rows(0, r0, r1, cudaMemcpyHostToDevice, sh);
         if (e == cudaSuccess) e = cudaEventRecord(ev_a[q], sh);
     }
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, ev_b, 0);
     for (int q = 0; q < npanel && e == cudaSuccess && st == LPY_OK; ++q) {
-        const int64_t r0 = q * prow, r1 = std::min(M, r0 + prow);
+        const int64_t r0 = pb[q], r1 = pb[q + 1];
         e = cudaStreamWaitEvent(sc, ev_a[q], 0);
         if (e != cudaSuccess) break;
         const bool arow = layout_a == LPY_ROW_MAJOR, crow = layout_c == LPY_ROW_MAJOR;
