@@ -216,14 +216,19 @@ __device__ __forceinline__ void load_b(const float *sb, int k, int wn, int ln, f
 // K-major tile (128 lines x 32 k, TMA 128B swizzle: 16-byte chunk c of line r
 // stored at chunk c ^ (r & 7)) -> MN-major [32 k][128] copy.  The tile is 8
 // k-chunks x 32 line-groups of 4x4 blocks; one warp pass covers 4 chunks x 8
-// line-groups (lane = chunk + 4 * group), so both the four LDS.128 (8 distinct
-// swizzled chunks per 128 B row pair) and the four STS.128 (8 distinct groups
-// per k row) move 512 B in 4 wavefronts, the minimum.
+// line-groups.  128-bit shared accesses are served a quarter-warp (8 lanes) at
+// a time, so each quarter must touch 8 distinct 16-byte bank groups on both
+// sides: lane l = lane & 7 of quarter k takes line-group g0 + l (distinct
+// groups for the STS.128 rows) and chunk c0 + ((l/2 + k) & 3) (4 chunks per
+// line-group parity, whose swizzles differ in bit 2, for the LDS.128) -- 4
+// wavefronts per 512 B on both sides.  (A lane = chunk + 4 * group mapping
+// stored with 16 wavefronts: ncu, profiles/r02_ffma_transpose_banks.txt.)
 template <int LINES>
 __device__ __forceinline__ void transpose_tile(const float *src, float *dst, int xw, int lane) {
     for (int it = xw; it < LINES / 16; it += XWARPS) {
-        const int c = (it & 1) * 4 + (lane & 3);
-        const int g = (it >> 1) * 8 + (lane >> 2);
+        const int l = lane & 7;
+        const int c = (it & 1) * 4 + (((l >> 1) + (lane >> 3)) & 3);
+        const int g = (it >> 1) * 8 + l;
         float4 r[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
