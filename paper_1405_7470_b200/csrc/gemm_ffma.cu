@@ -726,7 +726,7 @@ static cudaError_t launch_t(const Problem &p, const Knobs &kn, cudaStream_t s) {
         const int v = e ? atoi(e) : 0;
         return v >= 1 && v <= MAX_SPLITS ? v : 0;
     }();
-    if (force_splits) prm.splits = force_splits;
+    if (force_splits && force_splits <= prm.k_blocks) prm.splits = force_splits;   // (every slice non-empty)
     prm.num_units = prm.num_tiles * prm.splits;
     prm.ws = nullptr;
     prm.sem = nullptr;
