@@ -592,3 +592,22 @@ def test_b_multicast_cluster_mode(M, N, K, tmp_path):
     assert ((out["1"].double() - ref).abs() / D).max().item() <= TOL
     if K < 4096:
         assert torch.equal(out["0"], out["1"])
+
+
+def test_randomised_shapes_layouts_pads():
+    """Randomised sweep (scripts/fuzz_parity.py, 48 seeded cases): random shapes
+    from 1 to 3000 per dimension -- including wide ragged K-major ones that take
+    the 176-wide 3xTF32 tiles and the FFMA split-K / stream-K schedules, and long-K
+    ones -- random A/B/C layouts and leading-dimension pads (packed, unaligned,
+    aligned), both paths and auto; every element within the 1e-5 bound of a
+    float64 reference (cuBLAS DGEMM on the same inputs, a library cross-check)
+    and C's padding untouched.  (360 cases passed on B200 during development:
+    profiles/r02_fuzz.txt.)"""
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "fuzz_parity.py"), "48", "7"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().endswith("48 cases, 0 failures"), r.stdout[-3000:]
